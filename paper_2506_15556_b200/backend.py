@@ -1,0 +1,268 @@
+"""`B200LM`: the reference's `LanguageModel` surface backed by the CUDA runtime.
+
+Drop-in for `specstream.lm.LanguageModel` (`/root/reference/pkg/src/specstream/
+lm.py:157-213`): the reference's own `verify_greedy`, `ar_generate`,
+`greedy_decode` and `run_turn` run on it unchanged (tests/test_dropin_gpu.py),
+and this package's algorithm layer additionally uses the fused entry points
+`verify_greedy_fused` / `decode_greedy_fused` / `discard_after`.
+
+Semantics kept from the reference:
+
+* `forward(context, cache)` returns rows for every position not covered by
+  `cache`, row j scoring token j+1; a handle over the whole context; and the
+  cost. Handle checks raise `PrefixViolationError` (`lm.py:192-199`).
+* cache transparency (`SPEC.md:158`): rows are bit-identical whatever the
+  cache, because the device keeps one resident sequence, reuses its longest
+  common prefix, and every kernel is batch-invariant (csrc/layers.cu).
+
+Cost modes: "modeled" charges the reference's `LatencyModel` exactly
+(`lm.py:56-57`), so decisions and event logs are comparable bit-for-bit with
+the CPU oracle; "measured" charges the CUDA-event milliseconds of the work
+the device actually did (a prefix hit costs ~0).
+
+Rows are lazy: a `LazyRow` knows its argmax (computed on the device by the
+fused LM-head kernel) and materialises the fp32 logits only when something
+other than `np.argmax` touches it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native
+from .model_api import CacheHandle, LanguageModel, LatencyModel, LogitsBlock, PrefixViolationError
+from .shapes import MODE_BF16, DecoderShape
+from .vocab import SyntheticVocabulary, terminator_mask
+
+
+class LazyRow:
+    """One logits row: argmax known, fp32 values fetched from the device on demand."""
+
+    __slots__ = ("_lm", "_ctx", "_pos", "_argmax", "_values")
+
+    def __init__(self, lm: "B200LM", ctx: tuple, pos: int, argmax: int) -> None:
+        self._lm = lm
+        self._ctx = ctx
+        self._pos = pos
+        self._argmax = argmax
+        self._values = None
+
+    # np.argmax(row) dispatches here (numpy's _wrapfunc) — no transfer needed.
+    def argmax(self, axis=None, out=None, **kw):
+        if axis not in (None, 0, -1) or out is not None or kw:
+            return np.asarray(self).argmax(axis=axis, out=out, **kw)
+        return np.intp(self._argmax)
+
+    def _materialize(self) -> np.ndarray:
+        if self._values is None:
+            self._values = self._lm._row_values(self._ctx, self._pos)
+        return self._values
+
+    def __array__(self, dtype=None, copy=None):
+        v = self._materialize()
+        return v if dtype is None else v.astype(dtype)
+
+    def __len__(self) -> int:
+        return self._lm.vocab_size
+
+    def __getitem__(self, idx):
+        return self._materialize()[idx]
+
+    def __iter__(self):
+        return iter(self._materialize())
+
+    def __getattr__(self, name):
+        return getattr(self._materialize(), name)
+
+
+class _LazyRows:
+    def __init__(self, lm: "B200LM", ctx: tuple, first: int, argmax: list[int]) -> None:
+        self._rows = [LazyRow(lm, ctx, first + i, a) for i, a in enumerate(argmax)]
+
+    def __len__(self) -> int:
+        return len(self._rows)
+
+    def __getitem__(self, i):
+        return self._rows[i]
+
+    def __iter__(self):
+        return iter(self._rows)
+
+    def __array__(self, dtype=None, copy=None):
+        arr = np.stack([np.asarray(r) for r in self._rows])
+        return arr if dtype is None else arr.astype(dtype)
+
+
+class B200LM(LanguageModel):
+    def __init__(self, shape: DecoderShape, vocab=None, seed: int = 0, latency: LatencyModel | None = None,
+                 cost_mode: str = "modeled", device: int = 0, max_seq: int = 2048, use_graphs: bool = True,
+                 vocab_shards: int = 1, shard_rank: int = 0) -> None:
+        vocab = SyntheticVocabulary(shape.vocab) if vocab is None else vocab
+        if len(vocab) != shape.vocab:
+            raise ValueError(f"vocabulary has {len(vocab)} ids, decoder shape expects {shape.vocab}")
+        if cost_mode not in ("modeled", "measured"):
+            raise ValueError("cost_mode must be 'modeled' or 'measured'")
+        super().__init__(vocab, latency)
+        self.shape = shape
+        self.cost_mode = cost_mode
+        self._lib = _native.load()
+        self._h = ctypes.c_void_p()
+        cfg = _native.PsConfig()
+        sigma = 0.02 * math.sqrt(shape.hidden)
+        for name in ("vocab", "hidden", "layers", "heads", "kv_heads", "head_dim", "intermediate", "mode"):
+            setattr(cfg, name, int(getattr(shape, name)))
+        cfg.tied_embeddings = int(shape.tied_embeddings)
+        cfg.qkv_bias = int(shape.qkv_bias)
+        cfg.rope_theta = shape.rope_theta
+        cfg.rms_eps = shape.rms_eps
+        cfg.term_bias = float(np.float32(shape.term_bias_sigma * sigma))
+        cfg.eos_bias = float(np.float32(shape.eos_bias_sigma * sigma))
+        cfg.seed = seed
+        cfg.max_seq = max_seq
+        cfg.device = device
+        cfg.vocab_shards = vocab_shards
+        cfg.shard_rank = shard_rank
+        cfg.use_graphs = int(use_graphs)
+        self.seed = seed
+        self.max_seq = max_seq
+        _native.check(self._lib, self._lib.ps_create(ctypes.byref(cfg), ctypes.byref(self._h)), "ps_create")
+        mask = terminator_mask(vocab)
+        buf = (ctypes.c_uint8 * len(mask)).from_buffer_copy(mask)
+        self._call("ps_set_terminators", buf, len(mask))
+        self._step_ms = None  # EMA of measured decode-step time
+        self.last_verify_ms = 0.0
+        self.verify_ms: list[float] = []
+        self.decode_ms: list[float] = []
+
+    # -- plumbing -----------------------------------------------------------------
+    def _call(self, name: str, *args) -> None:
+        if not self._h:
+            raise RuntimeError("backend is closed")
+        _native.check(self._lib, getattr(self._lib, name)(self._h, *args), name)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.ps_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        st = _native.PsStats()
+        self._call("ps_get_stats", ctypes.byref(st))
+        return st.as_dict()
+
+    def resident(self) -> list[int]:
+        n = ctypes.c_int32()
+        buf = (ctypes.c_int32 * self.max_seq)()
+        self._call("ps_resident", buf, self.max_seq, ctypes.byref(n))
+        return list(buf[: n.value])
+
+    def read_weights(self, tid: int, offset: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.float32)
+        self._call("ps_read_weights", tid, offset, count, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        return out
+
+    def _cost(self, uncached: int, ms: float) -> float:
+        return self.latency.pass_cost(uncached) if self.cost_mode == "modeled" else float(ms)
+
+    def _row_values(self, ctx: tuple, pos: int) -> np.ndarray:
+        """fp32 logits of position `pos` given ctx[:pos+1] (re-established if rolled back)."""
+        res = self.resident()
+        if len(res) <= pos or tuple(res[: pos + 1]) != tuple(ctx[: pos + 1]):
+            # batch invariance makes the recomputed row bit-identical
+            self._sync(list(ctx[: pos + 1]), pos + 1)
+        out = np.empty(self.vocab_size, dtype=np.float32)
+        self._call("ps_logits_rows", pos, 1, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        return out
+
+    def _sync(self, context: list[int], row_from: int):
+        n = len(context)
+        toks = _native.i32_array(context)
+        am = (ctypes.c_int32 * max(n - row_from, 1))()
+        computed = ctypes.c_int32()
+        ms = ctypes.c_float()
+        self._call("ps_forward", toks, n, row_from, am, ctypes.byref(computed), ctypes.byref(ms))
+        return list(am[: n - row_from]), computed.value, ms.value
+
+    # -- LanguageModel surface ---------------------------------------------------------
+    def forward(self, context, cache=None):
+        start = self._cached_start(context, cache)
+        ctx = tuple(int(t) for t in context)
+        argmax, _, ms = self._sync(list(ctx), start)
+        rows = _LazyRows(self, ctx, start, argmax)
+        return LogitsBlock(rows, start), CacheHandle(ctx, self._backend_id), self._cost(len(ctx) - start, ms)
+
+    # -- fused fast paths (used by this package's verifier / generator) ------------------
+    def verify_greedy_fused(self, prompt, candidate):
+        """One fused pass: (k, handle over prompt ++ candidate, cost)."""
+        if not prompt:
+            raise ValueError("verification requires a nonempty prompt context")
+        p = _native.i32_array(prompt)
+        c = _native.i32_array(candidate)
+        k = ctypes.c_int32()
+        term = ctypes.c_int32()
+        ms = ctypes.c_float()
+        self._call("ps_verify_greedy", p, len(prompt), c, len(candidate), ctypes.byref(k), ctypes.byref(term),
+                   None, ctypes.byref(ms))
+        self.last_verify_ms = ms.value
+        self.verify_ms.append(ms.value)
+        seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)
+        return k.value, CacheHandle(seq, self._backend_id), self._cost(len(seq), ms.value)
+
+    def verify_greedy_detail(self, prompt, candidate) -> dict:
+        """Fused verify returning every device output (tests / diagnostics)."""
+        p = _native.i32_array(prompt)
+        c = _native.i32_array(candidate)
+        k, term, ms = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_float()
+        am = (ctypes.c_int32 * (len(candidate) + 1))()
+        self._call("ps_verify_greedy", p, len(prompt), c, len(candidate), ctypes.byref(k), ctypes.byref(term),
+                   am, ctypes.byref(ms))
+        return {"k": k.value, "first_term": term.value, "argmax": list(am), "gpu_ms": ms.value}
+
+    def decode_greedy_fused(self, seq, n: int):
+        """Up to n greedy tokens continuing `seq` (stops after EOS): [(token, cost_ms)]."""
+        if n <= 0:
+            return []
+        s = _native.i32_array(seq)
+        out = (ctypes.c_int32 * n)()
+        ms = (ctypes.c_float * n)()
+        got = ctypes.c_int32()
+        self._call("ps_decode_greedy", s, len(seq), n, 1, out, ctypes.byref(got), ms)
+        steps = []
+        for i in range(got.value):
+            cost = self._cost(1, ms[i])
+            steps.append((int(out[i]), cost))
+            if i > 0 or ms[i] > 0:
+                self.decode_ms.append(ms[i])
+        if got.value > 1:
+            tail = [ms[i] for i in range(1, got.value)]
+            avg = sum(tail) / len(tail)
+            self._step_ms = avg if self._step_ms is None else 0.8 * self._step_ms + 0.2 * avg
+        return steps
+
+    def discard_after(self, n: int) -> None:
+        self._call("ps_truncate", int(n))
+
+    def decode_cost_estimate(self) -> float:
+        if self.cost_mode == "modeled":
+            return self.latency.pass_cost(1)
+        return self._step_ms if self._step_ms is not None else 1.0
+
+    def profile_decode(self, steps: int = 4) -> dict:
+        ms = (ctypes.c_double * 8)()
+        by = (ctypes.c_double * 8)()
+        self._call("ps_profile_decode", steps, ms, by)
+        names = ["embed_norms", "qkv_gemm", "attention", "o_gemm", "gate_up_gemm", "down_gemm", "lm_head", "other"]
+        return {n: {"ms": ms[i], "bytes": by[i]} for i, n in enumerate(names)}
+
+    @property
+    def is_bf16(self) -> bool:
+        return self.shape.mode == MODE_BF16

@@ -1,0 +1,399 @@
+// Row-parallel kernels around the GEMMs: embedding + RMSNorm, split-K
+// reduction fused with bias/RoPE/KV-append, paged causal attention,
+// residual + RMSNorm, SwiGLU, argmax reduction and the greedy-verify compare.
+//
+// Batch invariance (what keeps greedy speculation lossless):
+// every output element is produced by an arithmetic sequence that depends
+// only on its own row and absolute position — never on how many rows share
+// the pass. Split-K boundaries depend on (N, K) only and partials are summed
+// in split order; attention splits at absolute 64-token page boundaries and
+// combines them in order. A row computed inside a 72-row verify pass is
+// therefore bit-identical to the same row computed by a 1-row decode step.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ps {
+
+// ---------------------------------------------------------------------------
+// embedding gather + first RMSNorm (one CTA per row)
+// decode mode (tok_in == nullptr): the row's token is the argmax of the
+// previous position, so consecutive graph replays chain on the device.
+template <typename T>
+__global__ void __launch_bounds__(256) embed_norm_kernel(PassCtx* ctx, const int* __restrict__ tok_in,
+                                                         int* __restrict__ tokens_dev,
+                                                         const int* __restrict__ argmax_pos,
+                                                         const T* __restrict__ embed, float* __restrict__ x,
+                                                         T* __restrict__ xn, int H, float eps) {
+  __shared__ float red[32];
+  __shared__ int s_tok;
+  const int t = blockIdx.x;
+  if (ctx->stop || t >= ctx->rows) return;
+  const int pos = ctx->n0 + t;
+  if (threadIdx.x == 0) {
+    int tok;
+    if (tok_in) {
+      tok = tok_in[t];
+    } else {
+      tok = argmax_pos[pos - 1];
+      if (ctx->stop_on_eos && tok == kEos) ctx->stop = 1;
+    }
+    tokens_dev[pos] = tok;
+    s_tok = tok;
+  }
+  __syncthreads();
+  if (ctx->stop) return;
+  const T* e = embed + size_t(s_tok) * H;
+  float* xr = x + size_t(t) * H;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < H; c += 256) {
+    float v = ld_as_f32(e + c);
+    xr[c] = v;
+    ss = fmaf(v, v, ss);
+  }
+  ss = block_sum<256>(ss, red);
+  const float rstd = 1.0f / sqrtf(ss / float(H) + eps);
+  T* o = xn + size_t(t) * H;
+  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(xr[c] * rstd);
+}
+
+template <typename T>
+void launch_embed_norm(const PassCtx* ctx, int max_rows, const int* tok_in, int* tokens_dev,
+                       const int* argmax_pos, const T* embed, float* x, T* xn, int hidden, float eps,
+                       cudaStream_t st) {
+  embed_norm_kernel<T><<<max_rows, 256, 0, st>>>(const_cast<PassCtx*>(ctx), tok_in, tokens_dev,
+                                                  argmax_pos, embed, x, xn, hidden, eps);
+}
+
+// ---------------------------------------------------------------------------
+// split-K sum + bias + RoPE (rotate-half) + q store + paged K/V append
+template <typename T>
+__global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __restrict__ ctx,
+                                                           const float* __restrict__ part, int splits,
+                                                           int N, const T* __restrict__ bias,
+                                                           const float2* __restrict__ rope, T* __restrict__ q,
+                                                           T* __restrict__ kpool, T* __restrict__ vpool,
+                                                           const int* __restrict__ page_table, KvGeom g,
+                                                           int layer, int heads) {
+  const int t = blockIdx.x;
+  if (ctx->stop || t >= ctx->rows) return;
+  const int pos = ctx->n0 + t;
+  const int hd = g.head_dim, half = hd >> 1;
+  const int nq = heads * half, nk = g.kv_heads * half;
+  const size_t sstride = size_t(kMaxWindow) * N;
+  const float* pr = part + size_t(t) * N;
+  auto sum_col = [&](int c) {
+    float v = pr[c];
+    for (int s = 1; s < splits; ++s) v += pr[s * sstride + c];
+    if (bias) v += ld_as_f32(bias + c);
+    return v;
+  };
+  const size_t page = size_t(page_table[pos / kPage]);
+  const int slot = pos % kPage;
+  const size_t lbase = size_t(layer) * g.layer_stride();
+  for (int p = threadIdx.x; p < nq + 2 * nk; p += blockDim.x) {
+    if (p < nq + nk) {
+      const bool is_q = p < nq;
+      const int pp = is_q ? p : p - nq;
+      const int h = pp / half, i = pp % half;
+      const int col = (is_q ? 0 : heads * hd) + h * hd + i;
+      const float a = sum_col(col), b = sum_col(col + half);
+      const float2 cs = rope[size_t(pos) * half + i];
+      const float ra = a * cs.x - b * cs.y;
+      const float rb = b * cs.x + a * cs.y;
+      if (is_q) {
+        T* qr = q + size_t(t) * heads * hd + h * hd;
+        qr[i] = from_f32<T>(ra);
+        qr[i + half] = from_f32<T>(rb);
+      } else {
+        T* kr = kpool + lbase + ((page * g.kv_heads + h) * kPage + slot) * hd;
+        kr[i] = from_f32<T>(ra);
+        kr[i + half] = from_f32<T>(rb);
+      }
+    } else {
+      const int pp = p - nq - nk;  // v pairs: write two plain elements
+      const int h = pp / half, i = pp % half;
+      const int col = (heads + g.kv_heads) * hd + h * hd + i;
+      T* vr = vpool + lbase + ((page * g.kv_heads + h) * kPage + slot) * hd;
+      vr[i] = from_f32<T>(sum_col(col));
+      vr[i + half] = from_f32<T>(sum_col(col + half));
+    }
+  }
+}
+
+template <typename T>
+void launch_qkv_finalize(const PassCtx* ctx, int max_rows, const float* part, int splits, int ldp,
+                         const T* bias, const float2* rope, T* q, T* kpool, T* vpool,
+                         const int* page_table, KvGeom g, int layer, int heads, cudaStream_t st) {
+  qkv_finalize_kernel<T><<<max_rows, 128, 0, st>>>(ctx, part, splits, ldp, bias, rope, q, kpool, vpool,
+                                                   page_table, g, layer, heads);
+}
+
+// ---------------------------------------------------------------------------
+// causal attention over the paged prefix. CTA = (query row, kv head, page);
+// one warp per query head of the GQA group. Scores: lane j owns keys j and
+// j+32 of the page; values: lane owns head dims lane, lane+32, ...
+template <typename T>
+__global__ void attention_page_kernel(const PassCtx* __restrict__ ctx, const T* __restrict__ q,
+                                      const T* __restrict__ kpool, const T* __restrict__ vpool,
+                                      const int* __restrict__ page_table, KvGeom g, int layer, int heads,
+                                      int max_splits, float scale, float* __restrict__ o_part,
+                                      float* __restrict__ ml_part) {
+  extern __shared__ float sm[];
+  const int t = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+  if (ctx->stop || t >= ctx->rows) return;
+  const int pos = ctx->n0 + t;
+  if (s > pos / kPage) return;
+  const int hd = g.head_dim, grp = heads / g.kv_heads;
+  const int nkeys = min(kPage, pos + 1 - s * kPage);
+  float* Ks = sm;                       // [64][hd+1]
+  float* Vs = Ks + kPage * (hd + 1);    // [64][hd]
+  float* Qs = Vs + kPage * hd;          // [grp][hd]
+  const size_t page = size_t(page_table[s]);
+  const size_t off = size_t(layer) * g.layer_stride() + (page * g.kv_heads + kvh) * kPage * hd;
+  for (int e = threadIdx.x; e < nkeys * hd; e += blockDim.x) {
+    const int j = e / hd, d = e % hd;
+    Ks[j * (hd + 1) + d] = ld_as_f32(kpool + off + e);
+    Vs[j * hd + d] = ld_as_f32(vpool + off + e);
+  }
+  const T* qrow = q + size_t(t) * heads * hd + size_t(kvh) * grp * hd;
+  for (int e = threadIdx.x; e < grp * hd; e += blockDim.x) Qs[e] = ld_as_f32(qrow + e);
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w >= grp) return;
+  const float* qs = Qs + w * hd;
+  float sc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int j = lane + 32 * r;
+    float acc = 0.f;
+    if (j < nkeys) {
+      const float* kr = Ks + j * (hd + 1);
+      for (int d = 0; d < hd; ++d) acc = fmaf(qs[d], kr[d], acc);
+      sc[r] = acc * scale;
+    } else {
+      sc[r] = -INFINITY;
+    }
+  }
+  const float m = warp_max(fmaxf(sc[0], sc[1]));
+  const float p0 = (lane < nkeys) ? expf(sc[0] - m) : 0.f;
+  const float p1 = (lane + 32 < nkeys) ? expf(sc[1] - m) : 0.f;
+  const float l = warp_sum(p0 + p1);
+  const int h = kvh * grp + w;
+  const size_t slot = (size_t(t) * heads + h) * max_splits + s;
+  for (int d = lane; d < hd; d += 32) {
+    float acc = 0.f;
+    for (int j = 0; j < nkeys; ++j) {
+      const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
+      acc = fmaf(pj, Vs[j * hd + d], acc);
+    }
+    o_part[slot * hd + d] = acc;
+  }
+  if (lane == 0) {
+    ml_part[slot * 2] = m;
+    ml_part[slot * 2 + 1] = l;
+  }
+}
+
+template <typename T>
+__global__ void attention_combine_kernel(const PassCtx* __restrict__ ctx, int heads, int hd, int max_splits,
+                                         const float* __restrict__ o_part, const float* __restrict__ ml_part,
+                                         T* __restrict__ out) {
+  const int t = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  if (ctx->stop || t >= ctx->rows) return;
+  const int nsplit = (ctx->n0 + t) / kPage + 1;
+  const size_t base = (size_t(t) * heads + h) * max_splits;
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ml_part[(base + s) * 2]);
+  float L = 0.f, acc = 0.f;
+  for (int s = 0; s < nsplit; ++s) {
+    const float f = expf(ml_part[(base + s) * 2] - M);
+    L = fmaf(ml_part[(base + s) * 2 + 1], f, L);
+    acc = fmaf(o_part[(base + s) * hd + d], f, acc);
+  }
+  out[size_t(t) * heads * hd + size_t(h) * hd + d] = from_f32<T>(acc / L);
+}
+
+template <typename T>
+void launch_attention(const PassCtx* ctx, int max_rows, int max_pos, const T* q, const T* kpool,
+                      const T* vpool, const int* page_table, KvGeom g, int layer, int heads,
+                      float* o_part, float* ml_part, T* attn_out, cudaStream_t st) {
+  const int max_splits = max_pos / kPage + 1;
+  const int grp = heads / g.kv_heads;
+  const int hd = g.head_dim;
+  const size_t smem = (size_t(kPage) * (hd + 1) + size_t(kPage) * hd + size_t(grp) * hd) * sizeof(float);
+  static bool attr_set[2] = {false, false};
+  const int key = sizeof(T) == 4 ? 0 : 1;
+  if (!attr_set[key]) {
+    cudaFuncSetAttribute(attention_page_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr_set[key] = true;
+  }
+  const float scale = float(1.0 / sqrt(double(hd)));
+  dim3 grid(max_rows, g.kv_heads, max_splits);
+  attention_page_kernel<T><<<grid, grp * 32, smem, st>>>(ctx, q, kpool, vpool, page_table, g, layer, heads,
+                                                         max_splits, scale, o_part, ml_part);
+  attention_combine_kernel<T><<<dim3(max_rows, heads), hd, 0, st>>>(ctx, heads, hd, max_splits, o_part,
+                                                                     ml_part, attn_out);
+}
+
+// ---------------------------------------------------------------------------
+// x += sum_s part[s]; then RMSNorm -> xn (next GEMM input) or, after the last
+// layer, -> hn_cache[pos] (LM-head input, kept per position for lazy rows).
+template <typename T>
+__global__ void __launch_bounds__(256) residual_norm_kernel(const PassCtx* __restrict__ ctx, float* __restrict__ x,
+                                                            const float* __restrict__ part, int splits,
+                                                            T* __restrict__ xn, T* __restrict__ hn_cache, int H,
+                                                            float eps) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  if (ctx->stop || t >= ctx->rows) return;
+  const size_t sstride = size_t(kMaxWindow) * H;
+  float* xr = x + size_t(t) * H;
+  const float* pr = part + size_t(t) * H;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < H; c += 256) {
+    float d = pr[c];
+    for (int s = 1; s < splits; ++s) d += pr[s * sstride + c];
+    const float v = xr[c] + d;
+    xr[c] = v;
+    ss = fmaf(v, v, ss);
+  }
+  ss = block_sum<256>(ss, red);
+  const float rstd = 1.0f / sqrtf(ss / float(H) + eps);
+  T* o = hn_cache ? hn_cache + size_t(ctx->n0 + t) * H : xn + size_t(t) * H;
+  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(xr[c] * rstd);
+}
+
+template <typename T>
+void launch_residual_norm(const PassCtx* ctx, int max_rows, float* x, const float* part, int splits,
+                          int ldp, T* xn, T* hn_cache, int hidden, float eps, cudaStream_t st) {
+  (void)ldp;
+  residual_norm_kernel<T><<<max_rows, 256, 0, st>>>(ctx, x, part, splits, xn, hn_cache, hidden, eps);
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void swiglu_kernel(const PassCtx* __restrict__ ctx, const float* __restrict__ part, int splits,
+                              T* __restrict__ act, int I) {
+  const int t = blockIdx.y;
+  if (ctx->stop || t >= ctx->rows) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const int N = 2 * I;
+  const size_t sstride = size_t(kMaxWindow) * N;
+  const float* pr = part + size_t(t) * N;
+  float gsum = pr[i], usum = pr[I + i];
+  for (int s = 1; s < splits; ++s) {
+    gsum += pr[s * sstride + i];
+    usum += pr[s * sstride + I + i];
+  }
+  const float silu = gsum / (1.0f + expf(-gsum));
+  act[size_t(t) * I + i] = from_f32<T>(silu * usum);
+}
+
+template <typename T>
+void launch_swiglu(const PassCtx* ctx, int max_rows, const float* part, int splits, int ldp, T* act,
+                   int inter, cudaStream_t st) {
+  (void)ldp;
+  swiglu_kernel<T><<<dim3((inter + 255) / 256, max_rows), 256, 0, st>>>(ctx, part, splits, act, inter);
+}
+
+// ---------------------------------------------------------------------------
+// argmax over vocab-tile partials; ties -> lowest id (merge is a total order,
+// so the result does not depend on reduction order).
+__global__ void __launch_bounds__(256) argmax_reduce_kernel(PassCtx* ctx, const float* __restrict__ am_val,
+                                                            const int* __restrict__ am_idx, int tiles,
+                                                            int* __restrict__ argmax_pos,
+                                                            unsigned long long* __restrict__ packed_out) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  const int t = blockIdx.x;
+  if (ctx->stop || t >= ctx->rows) return;
+  float v = -INFINITY;
+  int i = 0x7fffffff;
+  for (int k = threadIdx.x; k < tiles; k += 256)
+    argmax_merge(v, i, am_val[size_t(k) * kMaxWindow + t], am_idx[size_t(k) * kMaxWindow + t]);
+  warp_argmax(v, i);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sv[w] = v; si[w] = i; }
+  __syncthreads();
+  if (w == 0) {
+    v = l < 8 ? sv[l] : -INFINITY;
+    i = l < 8 ? si[l] : 0x7fffffff;
+    warp_argmax(v, i);
+    if (l == 0) {
+      argmax_pos[ctx->n0 + t] = i;
+      if (packed_out) {
+        // orderable float key in the high word, (0xFFFFFFFF - id) low: a
+        // uint64 MAX across vocab shards yields (max value, lowest id).
+        unsigned u = __float_as_uint(v);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        packed_out[t] = (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFull - unsigned(i));
+      }
+    }
+  }
+}
+
+void launch_argmax_reduce(const PassCtx* ctx, int max_rows, const float* am_val, const int* am_idx,
+                          int tiles, int* argmax_pos, unsigned long long* packed_out, cudaStream_t st) {
+  argmax_reduce_kernel<<<max_rows, 256, 0, st>>>(const_cast<PassCtx*>(ctx), am_val, am_idx, tiles, argmax_pos,
+                                                 packed_out);
+}
+
+// ---------------------------------------------------------------------------
+// greedy verify epilogue (one warp): accept length + first terminator of R.
+__global__ void verify_compare_kernel(const int* __restrict__ argmax_pos, int p0, const int* __restrict__ cand,
+                                      int n_cand, const unsigned char* __restrict__ term_mask,
+                                      int* __restrict__ res) {
+  const int lane = threadIdx.x;
+  int k = n_cand, first_term = -1;
+  for (int base = 0; base < n_cand; base += 32) {
+    const int i = base + lane;
+    bool miss = false, term = false;
+    if (i < n_cand) {
+      const int tok = cand[i];
+      miss = argmax_pos[p0 - 1 + i] != tok;
+      term = term_mask[tok] != 0;
+    }
+    const unsigned mb = __ballot_sync(0xffffffffu, miss);
+    const unsigned tb = __ballot_sync(0xffffffffu, term);
+    if (first_term < 0 && tb) first_term = base + __ffs(tb) - 1;
+    if (mb) { k = base + __ffs(mb) - 1; break; }
+  }
+  // keep scanning for the terminator past the mismatch
+  if (first_term < 0) {
+    for (int base = (k / 32) * 32; base < n_cand; base += 32) {
+      const int i = base + lane;
+      const bool term = i < n_cand && term_mask[cand[i]] != 0;
+      const unsigned tb = __ballot_sync(0xffffffffu, term);
+      if (tb) { first_term = base + __ffs(tb) - 1; break; }
+    }
+  }
+  if (lane == 0) { res[0] = k; res[1] = first_term; }
+}
+
+void launch_verify_compare(const int* argmax_pos, int p0, const int* cand, int n_cand,
+                           const unsigned char* term_mask, int* res, cudaStream_t st) {
+  verify_compare_kernel<<<1, 32, 0, st>>>(argmax_pos, p0, cand, n_cand, term_mask, res);
+}
+
+__global__ void advance_kernel(PassCtx* ctx) {
+  if (!ctx->stop) { ctx->n0 += 1; ctx->step += 1; }
+}
+
+void launch_advance(PassCtx* ctx, cudaStream_t st) { advance_kernel<<<1, 1, 0, st>>>(ctx); }
+
+#define PS_INST(T)                                                                                       \
+  template void launch_embed_norm<T>(const PassCtx*, int, const int*, int*, const int*, const T*, float*, \
+                                     T*, int, float, cudaStream_t);                                     \
+  template void launch_qkv_finalize<T>(const PassCtx*, int, const float*, int, int, const T*,           \
+                                       const float2*, T*, T*, T*, const int*, KvGeom, int, int,          \
+                                       cudaStream_t);                                                    \
+  template void launch_attention<T>(const PassCtx*, int, int, const T*, const T*, const T*, const int*,  \
+                                    KvGeom, int, int, float*, float*, T*, cudaStream_t);                 \
+  template void launch_residual_norm<T>(const PassCtx*, int, float*, const float*, int, int, T*, T*, int, \
+                                        float, cudaStream_t);                                            \
+  template void launch_swiglu<T>(const PassCtx*, int, const float*, int, int, T*, int, cudaStream_t);
+PS_INST(float)
+PS_INST(__nv_bfloat16)
+
+}  // namespace ps

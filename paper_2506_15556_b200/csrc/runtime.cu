@@ -1,0 +1,876 @@
+// C-ABI runtime (include/predgen_b200.h): weights, paged KV, passes, decode graph.
+//
+// Host control flow per call is deliberately thin: token ids in, argmax ids /
+// accept length out, one stream, one synchronisation at the end of each call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "predgen_b200.h"
+
+using namespace ps;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail(PS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// weight tensor ids (oracle/weights.py)
+constexpr int TID_EMBED = 1, TID_HEAD = 2;
+constexpr int WQ = 0, WK = 1, WV = 2, WO = 3, WGATE = 4, WUP = 5, WDOWN = 6, BQ = 7, BK = 8, BV = 9;
+int layer_tid(int l, int w) { return 64 + 16 * l + w; }
+
+struct Gemm {
+  void* w = nullptr;
+  int N = 0, K = 0, splits = 1;
+  TmaDesc tm;
+};
+
+struct Layer {
+  Gemm qkv, o, gu, d;
+  void* bqkv = nullptr;
+};
+
+struct ActDescs {
+  TmaDesc xn, attn, act, hn;
+};
+
+struct WEntry {
+  int tid;
+  void* ptr;
+  int64_t count;
+};
+
+constexpr int kCtxSlots = 64;
+constexpr int kMaxSteps = 256;
+constexpr int kProfClasses = 8;
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+int choose_splits(int N, int K, int tile_n, int kgran, int max_ksplit) {
+  const int tiles = N / tile_n;
+  int s = 1;
+  while (tiles * s < 2 * 148 && K % (2 * s * kgran) == 0 && K / (2 * s) >= 512) s *= 2;
+  while (max_ksplit > 0 && K / s > max_ksplit && K % (2 * s * kgran) == 0) s *= 2;
+  return s;
+}
+
+}  // namespace
+
+struct Prof {
+  cudaEvent_t ev[2 * 40 * 12 + 8];
+  int n = 0;
+  int cls[2 * 40 * 12 + 8];
+};
+
+struct ps_handle {
+  ps_config cfg{};
+  bool bf16 = false;
+  size_t esz = 4;
+  cudaStream_t st = nullptr;
+  std::vector<void*> allocs;
+  std::vector<void*> host_allocs;
+
+  int H = 0, V = 0, L = 0, nh = 0, nkv = 0, hd = 0, I = 0, qd = 0, kvd = 0;
+  int v_begin = 0, v_count = 0;
+
+  void* embed = nullptr;
+  void* head = nullptr;
+  float* lm_bias = nullptr;
+  std::vector<Layer> layers;
+  TmaDesc tm_head;
+  std::vector<WEntry> wreg;
+  double weight_bytes = 0;
+
+  void* kpool = nullptr;
+  void* vpool = nullptr;
+  KvGeom g{};
+  int* d_page_table = nullptr;
+  int* h_page_table = nullptr;  // pinned
+  std::vector<int> free_pages;
+  int pages_mapped = 0;
+
+  float* x = nullptr;
+  void* xn = nullptr;
+  void* q = nullptr;
+  void* attn = nullptr;
+  void* act = nullptr;
+  float* part = nullptr;
+  float* o_part = nullptr;
+  float* ml_part = nullptr;
+  void* hn_cache = nullptr;
+  float* am_val = nullptr;
+  int* am_idx = nullptr;
+  int am_tiles = 0;
+  int* argmax_pos = nullptr;
+  int* tokens_dev = nullptr;
+  unsigned char* term_mask = nullptr;
+  float2* rope = nullptr;
+  int* d_tok = nullptr;
+  int* d_cand = nullptr;
+  int* d_res = nullptr;
+  PassCtx* d_ctx = nullptr;
+  PassCtx* d_ctx_aux = nullptr;
+  float* logits_buf = nullptr;
+
+  PassCtx* h_ctx = nullptr;   // pinned ring [kCtxSlots]
+  int* h_tok = nullptr;       // pinned ring [kCtxSlots][kMaxWindow]
+  int* h_res = nullptr;       // pinned [4]
+  int* h_argmax = nullptr;    // pinned [max_seq + kMaxWindow]
+  int* h_steps_tok = nullptr; // pinned [kMaxSteps]
+  int ring = 0;
+
+  std::vector<int> resident;
+  std::vector<int> argmax_host;
+
+  std::map<int, ActDescs> act_tm;
+  cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> step_ev;
+  ps_stats stats{};
+  Prof* prof = nullptr;
+  bool prof_on = false;
+
+  template <typename T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, n * sizeof(T) + 256) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, n * sizeof(T) + 256);
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* halloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+    std::memset(p, 0, n * sizeof(T));
+    host_allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+
+void* alloc_weights(ps_handle* h, size_t count) {
+  return h->bf16 ? static_cast<void*>(h->dalloc<__nv_bfloat16>(count)) : static_cast<void*>(h->dalloc<float>(count));
+}
+
+void init_tensor(ps_handle* h, void* dst, uint64_t count, uint64_t first, int tid, bool registry = true) {
+  if (h->bf16)
+    launch_init_uniform(static_cast<__nv_bfloat16*>(dst), count, first, h->cfg.seed, tid, 0.02, h->st);
+  else
+    launch_init_uniform(static_cast<float*>(dst), count, first, h->cfg.seed, tid, 0.02, h->st);
+  if (registry) h->wreg.push_back({tid, dst, int64_t(count)});
+}
+
+void* offset_ptr(ps_handle* h, void* base, size_t elems) {
+  return static_cast<unsigned char*>(base) + elems * h->esz;
+}
+
+int map_pages(ps_handle* h, int n_tokens) {
+  const int need = (n_tokens + kPage - 1) / kPage;
+  if (need > h->g.pages) return fail(PS_ERR_CAPACITY, "context exceeds KV capacity (max_seq)");
+  const int first_new = h->pages_mapped;
+  while (h->pages_mapped < need) {
+    const int phys = h->free_pages.back();
+    h->free_pages.pop_back();
+    h->h_page_table[h->pages_mapped++] = phys;
+  }
+  if (need > first_new) {
+    CK(cudaMemcpyAsync(h->d_page_table + first_new, h->h_page_table + first_new, sizeof(int) * (need - first_new),
+                       cudaMemcpyHostToDevice, h->st));
+  }
+  h->stats.kv_pages_used = h->pages_mapped;
+  return PS_OK;
+}
+
+void truncate_to(ps_handle* h, int n) {
+  if (n >= int(h->resident.size())) return;
+  h->stats.rollbacks += 1;
+  h->resident.resize(n);
+  h->argmax_host.resize(n);
+  const int keep = (n + kPage - 1) / kPage;
+  while (h->pages_mapped > keep) h->free_pages.push_back(h->h_page_table[--h->pages_mapped]);
+  h->stats.kv_tokens = n;
+  h->stats.kv_pages_used = h->pages_mapped;
+}
+
+const ActDescs* act_descs(ps_handle* h, int ntok) {
+  auto it = h->act_tm.find(ntok);
+  if (it != h->act_tm.end()) return &it->second;
+  ActDescs d;
+  bool ok = encode_tma_2d_bf16(&d.xn, h->xn, h->H, kMaxWindow, 64, ntok);
+  ok = ok && encode_tma_2d_bf16(&d.attn, h->attn, h->qd, kMaxWindow, 64, ntok);
+  ok = ok && encode_tma_2d_bf16(&d.act, h->act, h->I, kMaxWindow, 64, ntok);
+  ok = ok && encode_tma_2d_bf16(&d.hn, h->hn_cache, h->H, h->cfg.max_seq + kMaxWindow, 64, ntok);
+  if (!ok) return nullptr;
+  return &h->act_tm.emplace(ntok, d).first->second;
+}
+
+void prof_mark(ps_handle* h, int cls) {
+  Prof* p = h->prof;
+  if (!p || !h->prof_on) return;
+  cudaEventRecord(p->ev[p->n], h->st);
+  p->cls[p->n] = cls;
+  p->n++;
+}
+
+// One forward pass of the decoder body + LM head + argmax over `max_rows`
+// rows at ctx->n0 (device-side). tok_in == nullptr selects decode mode.
+template <typename T>
+void enqueue_pass(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
+  cudaStream_t st = h->st;
+  const int ntok = round_up(std::max(max_rows, 1), 16);
+  const ActDescs* ad = h->bf16 ? act_descs(h, ntok) : nullptr;
+  T* xn = static_cast<T*>(h->xn);
+  T* qb = static_cast<T*>(h->q);
+  T* attn = static_cast<T*>(h->attn);
+  T* act = static_cast<T*>(h->act);
+  T* hn = static_cast<T*>(h->hn_cache);
+  auto gemm = [&](const Gemm& gm, const void* X, const TmaDesc* tmx) {
+    if (h->bf16)
+      launch_gemm_tc(ctx, &gm.tm, tmx, h->part, gm.N, gm.K, gm.splits, ntok, 0, st);
+    else
+      launch_gemm_f32(ctx, max_rows, static_cast<const float*>(X), gm.K, static_cast<const float*>(gm.w), h->part,
+                      gm.N, gm.K, gm.splits, st);
+  };
+  prof_mark(h, 0);
+  launch_embed_norm<T>(ctx, max_rows, tok_in, h->tokens_dev, h->argmax_pos, static_cast<const T*>(h->embed), h->x, xn,
+                       h->H, h->cfg.rms_eps, st);
+  for (int l = 0; l < h->L; ++l) {
+    const Layer& ly = h->layers[l];
+    prof_mark(h, 1);
+    gemm(ly.qkv, xn, ad ? &ad->xn : nullptr);
+    prof_mark(h, 7);
+    launch_qkv_finalize<T>(ctx, max_rows, h->part, ly.qkv.splits, ly.qkv.N, static_cast<const T*>(ly.bqkv), h->rope,
+                           qb, static_cast<T*>(h->kpool), static_cast<T*>(h->vpool), h->d_page_table, h->g, l, h->nh,
+                           st);
+    prof_mark(h, 2);
+    launch_attention<T>(ctx, max_rows, max_pos, qb, static_cast<const T*>(h->kpool), static_cast<const T*>(h->vpool),
+                        h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part, attn, st);
+    prof_mark(h, 3);
+    gemm(ly.o, attn, ad ? &ad->attn : nullptr);
+    prof_mark(h, 0);
+    launch_residual_norm<T>(ctx, max_rows, h->x, h->part, ly.o.splits, h->H, xn, nullptr, h->H, h->cfg.rms_eps, st);
+    prof_mark(h, 4);
+    gemm(ly.gu, xn, ad ? &ad->xn : nullptr);
+    prof_mark(h, 7);
+    launch_swiglu<T>(ctx, max_rows, h->part, ly.gu.splits, ly.gu.N, act, h->I, st);
+    prof_mark(h, 5);
+    gemm(ly.d, act, ad ? &ad->act : nullptr);
+    prof_mark(h, 0);
+    launch_residual_norm<T>(ctx, max_rows, h->x, h->part, ly.d.splits, h->H, xn, l == h->L - 1 ? hn : nullptr, h->H,
+                            h->cfg.rms_eps, st);
+  }
+  prof_mark(h, 6);
+  if (h->bf16)
+    launch_lmhead_tc(ctx, &h->tm_head, &ad->hn, h->lm_bias, h->v_begin, h->v_count, h->H, ntok, 0, h->am_val,
+                     h->am_idx, nullptr, 0, st);
+  else
+    launch_lmhead_f32(ctx, max_rows, static_cast<const float*>(h->hn_cache), 0, static_cast<const float*>(h->head),
+                      h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val, h->am_idx, nullptr, 0, st);
+  launch_argmax_reduce(ctx, max_rows, h->am_val, h->am_idx, h->am_tiles, h->argmax_pos, nullptr, st);
+  prof_mark(h, 7);
+}
+
+void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
+  if (h->bf16)
+    enqueue_pass<__nv_bfloat16>(h, ctx, max_rows, tok_in, max_pos);
+  else
+    enqueue_pass<float>(h, ctx, max_rows, tok_in, max_pos);
+}
+
+PassCtx* next_ctx_slot(ps_handle* h, int* slot) {
+  *slot = h->ring;
+  h->ring = (h->ring + 1) % kCtxSlots;
+  return h->h_ctx + *slot;
+}
+
+// Append tokens[0..n) to the resident sequence: chunks of <= kMaxWindow rows.
+// Enqueue only; the caller synchronises and then calls finish_extend.
+int enqueue_extend(ps_handle* h, const int* tokens, int n, int* base_out) {
+  const int base = int(h->resident.size());
+  *base_out = base;
+  if (base + n > h->cfg.max_seq) return fail(PS_ERR_CAPACITY, "context exceeds KV capacity (max_seq)");
+  if (int rc = map_pages(h, base + n)) return rc;
+  for (int done = 0; done < n;) {
+    const int rows = std::min(kMaxWindow, n - done);
+    int slot;
+    PassCtx* hc = next_ctx_slot(h, &slot);
+    *hc = PassCtx{base + done, rows, 0, 0, 0, {0, 0, 0}};
+    int* ht = h->h_tok + size_t(slot) * kMaxWindow;
+    std::memcpy(ht, tokens + done, sizeof(int) * rows);
+    CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_tok, ht, sizeof(int) * rows, cudaMemcpyHostToDevice, h->st));
+    enqueue_pass_any(h, h->d_ctx, rows, h->d_tok, base + done + rows - 1);
+    CK(cudaGetLastError());
+    h->stats.passes += 1;
+    h->stats.rows += rows;
+    done += rows;
+  }
+  CK(cudaMemcpyAsync(h->h_argmax + base, h->argmax_pos + base, sizeof(int) * n, cudaMemcpyDeviceToHost, h->st));
+  return PS_OK;
+}
+
+void finish_extend(ps_handle* h, const int* tokens, int n, int base) {
+  h->resident.insert(h->resident.end(), tokens, tokens + n);
+  h->argmax_host.insert(h->argmax_host.end(), h->h_argmax + base, h->h_argmax + base + n);
+  h->stats.kv_tokens = int64_t(h->resident.size());
+}
+
+int lcp_with(const ps_handle* h, const int* tokens, int n) {
+  const int m = std::min(n, int(h->resident.size()));
+  int i = 0;
+  while (i < m && h->resident[i] == tokens[i]) ++i;
+  return i;
+}
+
+// Bring the resident sequence to exactly tokens[0..n) (rollback + extend).
+// Leaves the stream unsynchronised when *enqueued is set.
+// A context that is a prefix of the resident sequence costs nothing; the
+// longer resident tail is kept unless `exact` (decode must append at n).
+int sync_to(ps_handle* h, const int* tokens, int n, int* computed, int* base, bool* enqueued, bool exact) {
+  const int lcp = lcp_with(h, tokens, n);
+  *enqueued = false;
+  *computed = 0;
+  if (lcp == n) {
+    if (exact) truncate_to(h, n);
+    h->stats.prefix_hits += 1;
+    return PS_OK;
+  }
+  truncate_to(h, lcp);
+  if (int rc = enqueue_extend(h, tokens + lcp, n - lcp, base)) return rc;
+  *computed = n - lcp;
+  *enqueued = true;
+  return PS_OK;
+}
+
+int capture_decode_graph(ps_handle* h) {
+  if (h->graph) return PS_OK;
+  CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1);
+  launch_advance(h->d_ctx, h->st);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+  if (e != cudaSuccess) return fail(PS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&h->graph, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(PS_ERR_CUDA, std::string("decode graph instantiate: ") + cudaGetErrorString(e));
+  return PS_OK;
+}
+
+// `steps` 1-row decode steps starting at position n0 (device-chained).
+int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* executed, float* step_ms) {
+  if (n0 + steps > h->cfg.max_seq) return fail(PS_ERR_CAPACITY, "decode exceeds KV capacity (max_seq)");
+  if (int rc = map_pages(h, n0 + steps)) return rc;
+  int slot;
+  PassCtx* hc = next_ctx_slot(h, &slot);
+  *hc = PassCtx{n0, 1, 0, stop_at_eos, 0, {0, 0, 0}};
+  CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+  if (h->cfg.use_graphs) {
+    if (int rc = capture_decode_graph(h)) return rc;
+  }
+  while (int(h->step_ev.size()) < steps + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->step_ev.push_back(e);
+  }
+  CK(cudaEventRecord(h->step_ev[0], h->st));
+  for (int i = 0; i < steps; ++i) {
+    if (h->graph) {
+      CK(cudaGraphLaunch(h->graph, h->st));
+    } else {
+      enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1);
+      launch_advance(h->d_ctx, h->st);
+    }
+    CK(cudaEventRecord(h->step_ev[i + 1], h->st));
+  }
+  int s2;
+  PassCtx* back = next_ctx_slot(h, &s2);
+  CK(cudaMemcpyAsync(back, h->d_ctx, sizeof(PassCtx), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_argmax + n0, h->argmax_pos + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_steps_tok, h->tokens_dev + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaGetLastError());
+  *executed = back->step;
+  for (int i = 0; i < steps; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->step_ev[i], h->step_ev[i + 1]);
+    if (step_ms) step_ms[i] = ms;
+    h->stats.gpu_ms += ms;
+  }
+  h->stats.decode_steps += *executed;
+  h->stats.passes += *executed;
+  h->stats.rows += *executed;
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ps_last_error(void) { return g_err.c_str(); }
+
+int ps_create(const ps_config* cfg, ps_handle** out) {
+  if (!cfg || !out) return fail(PS_ERR_INVALID, "null argument");
+  *out = nullptr;
+  const ps_config& c = *cfg;
+  if (c.vocab <= 4 || c.hidden % 128 || c.head_dim % 64 || c.heads % c.kv_heads || c.intermediate % 128 ||
+      c.layers <= 0 || (c.mode != PS_MODE_F32 && c.mode != PS_MODE_BF16) || c.max_seq % kPage || c.max_seq <= 0)
+    return fail(PS_ERR_INVALID, "unsupported decoder shape");
+  const int shards = std::max(1, c.vocab_shards);
+  if (c.shard_rank < 0 || c.shard_rank >= shards) return fail(PS_ERR_INVALID, "bad shard rank");
+  CK(cudaSetDevice(c.device));
+  ps_handle* h = new ps_handle();
+  h->cfg = c;
+  h->bf16 = c.mode == PS_MODE_BF16;
+  h->esz = h->bf16 ? 2 : 4;
+  h->H = c.hidden;
+  h->V = c.vocab;
+  h->L = c.layers;
+  h->nh = c.heads;
+  h->nkv = c.kv_heads;
+  h->hd = c.head_dim;
+  h->I = c.intermediate;
+  h->qd = c.heads * c.head_dim;
+  h->kvd = c.kv_heads * c.head_dim;
+  // vocab shard: contiguous block, multiple of 128 ids except the last
+  const int per = round_up((c.vocab + shards - 1) / shards, 128);
+  h->v_begin = std::min(c.vocab, per * c.shard_rank);
+  h->v_count = std::min(c.vocab, h->v_begin + per) - h->v_begin;
+  if (h->bf16 && (h->qd % 128 || (2 * h->I) % 128))
+    return (delete h, fail(PS_ERR_INVALID, "bf16 mode needs 128-multiple projections"));
+  auto bad = [&](const char* what) {
+    ps_destroy(h);
+    return fail(PS_ERR_CUDA, std::string("allocation failed: ") + what);
+  };
+  if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
+  cudaEventCreate(&h->ev0);
+  cudaEventCreate(&h->ev1);
+
+  const int H = h->H, V = h->V, I = h->I, qd = h->qd, kvd = h->kvd;
+  // ---- weights (generated on device) ----
+  h->embed = alloc_weights(h, size_t(V) * H);
+  if (!h->embed) return bad("embedding");
+  init_tensor(h, h->embed, size_t(V) * H, 0, TID_EMBED);
+  if (c.tied_embeddings) {
+    h->head = offset_ptr(h, h->embed, size_t(h->v_begin) * H);
+  } else {
+    h->head = alloc_weights(h, size_t(h->v_count) * H);
+    if (!h->head) return bad("lm head");
+    init_tensor(h, h->head, size_t(h->v_count) * H, size_t(h->v_begin) * H, TID_HEAD, false);
+    h->wreg.push_back({TID_HEAD, h->head, int64_t(h->v_count) * H});
+  }
+  h->lm_bias = h->dalloc<float>(V);
+  {
+    std::vector<float> b(V, 0.f);
+    b[0] = c.eos_bias;
+    for (int i = 1; i < 4; ++i) b[i] = c.term_bias;
+    cudaMemcpy(h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
+  }
+  h->layers.resize(h->L);
+  const int tile_n = h->bf16 ? kTileTc : 16, kgran = h->bf16 ? 64 : 128, maxk = h->bf16 ? 0 : 2048;
+  size_t part_elems = 0;
+  for (int l = 0; l < h->L; ++l) {
+    Layer& ly = h->layers[l];
+    auto setup = [&](Gemm& gm, int N, int K) {
+      gm.N = N;
+      gm.K = K;
+      gm.splits = choose_splits(N, K, tile_n, kgran, maxk);
+      gm.w = alloc_weights(h, size_t(N) * K);
+      part_elems = std::max(part_elems, size_t(gm.splits) * kMaxWindow * N);
+      return gm.w != nullptr;
+    };
+    if (!setup(ly.qkv, qd + 2 * kvd, H) || !setup(ly.o, H, qd) || !setup(ly.gu, 2 * I, H) || !setup(ly.d, H, I))
+      return bad("layer weights");
+    init_tensor(h, ly.qkv.w, size_t(qd) * H, 0, layer_tid(l, WQ));
+    init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd) * H), size_t(kvd) * H, 0, layer_tid(l, WK));
+    init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd + kvd) * H), size_t(kvd) * H, 0, layer_tid(l, WV));
+    init_tensor(h, ly.o.w, size_t(H) * qd, 0, layer_tid(l, WO));
+    init_tensor(h, ly.gu.w, size_t(I) * H, 0, layer_tid(l, WGATE));
+    init_tensor(h, offset_ptr(h, ly.gu.w, size_t(I) * H), size_t(I) * H, 0, layer_tid(l, WUP));
+    init_tensor(h, ly.d.w, size_t(H) * I, 0, layer_tid(l, WDOWN));
+    if (c.qkv_bias) {
+      ly.bqkv = alloc_weights(h, size_t(qd + 2 * kvd));
+      if (!ly.bqkv) return bad("bias");
+      init_tensor(h, ly.bqkv, qd, 0, layer_tid(l, BQ));
+      init_tensor(h, offset_ptr(h, ly.bqkv, qd), kvd, 0, layer_tid(l, BK));
+      init_tensor(h, offset_ptr(h, ly.bqkv, qd + kvd), kvd, 0, layer_tid(l, BV));
+    }
+    if (h->bf16) {
+      bool ok = encode_tma_2d_bf16(&ly.qkv.tm, ly.qkv.w, H, ly.qkv.N, 64, kTileTc);
+      ok = ok && encode_tma_2d_bf16(&ly.o.tm, ly.o.w, qd, H, 64, kTileTc);
+      ok = ok && encode_tma_2d_bf16(&ly.gu.tm, ly.gu.w, H, 2 * I, 64, kTileTc);
+      ok = ok && encode_tma_2d_bf16(&ly.d.tm, ly.d.w, I, H, 64, kTileTc);
+      if (!ok) return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
+    }
+  }
+  h->weight_bytes = double(h->esz) * (double(h->L) * (double(qd + 2 * kvd) * H + double(H) * qd + 3.0 * H * I) +
+                                      double(h->v_count) * H);
+  h->stats.weight_bytes = h->weight_bytes;
+  if (h->bf16 && !encode_tma_2d_bf16(&h->tm_head, h->head, H, h->v_count, 64, kTileTc))
+    return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
+
+  // ---- paged KV pool ----
+  h->g = KvGeom{h->L, h->nkv, h->hd, c.max_seq / kPage};
+  const size_t kv_elems = size_t(h->L) * h->g.layer_stride();
+  h->kpool = alloc_weights(h, kv_elems);
+  h->vpool = alloc_weights(h, kv_elems);
+  h->d_page_table = h->dalloc<int>(h->g.pages);
+  h->h_page_table = h->halloc<int>(h->g.pages);
+  if (!h->kpool || !h->vpool || !h->d_page_table || !h->h_page_table) return bad("kv pool");
+  for (int p = h->g.pages - 1; p >= 0; --p) h->free_pages.push_back(p);
+
+  // ---- workspaces ----
+  const int max_splits_attn = c.max_seq / kPage + 1;
+  const size_t seq_rows = size_t(c.max_seq) + kMaxWindow;
+  h->x = h->dalloc<float>(size_t(kMaxWindow) * H);
+  h->xn = alloc_weights(h, size_t(kMaxWindow) * H);
+  h->q = alloc_weights(h, size_t(kMaxWindow) * qd);
+  h->attn = alloc_weights(h, size_t(kMaxWindow) * qd);
+  h->act = alloc_weights(h, size_t(kMaxWindow) * I);
+  h->part = h->dalloc<float>(part_elems);
+  h->o_part = h->dalloc<float>(size_t(kMaxWindow) * h->nh * max_splits_attn * h->hd);
+  h->ml_part = h->dalloc<float>(size_t(kMaxWindow) * h->nh * max_splits_attn * 2);
+  h->hn_cache = alloc_weights(h, seq_rows * H);
+  h->am_tiles = h->bf16 ? (h->v_count + kTileTc - 1) / kTileTc : (h->v_count + kLmTileF32 - 1) / kLmTileF32;
+  h->am_val = h->dalloc<float>(size_t(h->am_tiles) * kMaxWindow);
+  h->am_idx = h->dalloc<int>(size_t(h->am_tiles) * kMaxWindow);
+  h->argmax_pos = h->dalloc<int>(seq_rows);
+  h->tokens_dev = h->dalloc<int>(seq_rows);
+  h->term_mask = h->dalloc<unsigned char>(V);
+  h->rope = h->dalloc<float2>(seq_rows * (h->hd / 2));
+  h->d_tok = h->dalloc<int>(kMaxWindow);
+  h->d_cand = h->dalloc<int>(c.max_seq);
+  h->d_res = h->dalloc<int>(4);
+  h->d_ctx = h->dalloc<PassCtx>(1);
+  h->d_ctx_aux = h->dalloc<PassCtx>(1);
+  h->h_ctx = h->halloc<PassCtx>(kCtxSlots);
+  h->h_tok = h->halloc<int>(size_t(kCtxSlots) * kMaxWindow);
+  h->h_res = h->halloc<int>(4);
+  h->h_argmax = h->halloc<int>(seq_rows);
+  h->h_steps_tok = h->halloc<int>(std::max(kMaxSteps, c.max_seq));
+  if (!h->x || !h->xn || !h->q || !h->attn || !h->act || !h->part || !h->o_part || !h->ml_part || !h->hn_cache ||
+      !h->am_val || !h->am_idx || !h->argmax_pos || !h->tokens_dev || !h->term_mask || !h->rope || !h->d_tok ||
+      !h->d_cand || !h->d_res || !h->d_ctx || !h->d_ctx_aux || !h->h_ctx || !h->h_tok || !h->h_res ||
+      !h->h_argmax || !h->h_steps_tok)
+    return bad("workspace");
+  {
+    // RoPE table (rotate-half pairs): angle = pos * theta^(-2i/hd), in fp64.
+    const int half = h->hd / 2;
+    std::vector<float2> tab(seq_rows * half);
+    for (size_t p = 0; p < seq_rows; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(double(c.rope_theta), -(2.0 * i) / double(h->hd));
+        const double a = double(p) * inv;
+        tab[p * half + i] = make_float2(float(std::cos(a)), float(std::sin(a)));
+      }
+    cudaMemcpy(h->rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice);
+    std::vector<unsigned char> tm(V, 0);
+    tm[1] = tm[2] = tm[3] = 1;
+    cudaMemcpy(h->term_mask, tm.data(), V, cudaMemcpyHostToDevice);
+  }
+  if (cudaStreamSynchronize(h->st) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return (ps_destroy(h), fail(PS_ERR_CUDA, "device initialisation failed"));
+  *out = h;
+  return PS_OK;
+}
+
+void ps_destroy(ps_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->cfg.device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (auto e : h->step_ev) cudaEventDestroy(e);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  for (void* p : h->allocs) cudaFree(p);
+  for (void* p : h->host_allocs) cudaFreeHost(p);
+  if (h->logits_buf) cudaFree(h->logits_buf);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h->prof;
+  delete h;
+}
+
+int ps_forward(ps_handle* h, const int32_t* tokens, int32_t n, int32_t row_from, int32_t* argmax_out,
+               int32_t* computed_out, float* gpu_ms) {
+  if (!h || !tokens || n <= 0 || row_from < 0 || row_from > n) return fail(PS_ERR_INVALID, "bad forward arguments");
+  CK(cudaSetDevice(h->cfg.device));
+  int computed = 0, base = 0;
+  bool enq = false;
+  CK(cudaEventRecord(h->ev0, h->st));
+  if (int rc = sync_to(h, tokens, n, &computed, &base, &enq, false)) return rc;
+  CK(cudaEventRecord(h->ev1, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaGetLastError());
+  if (enq) finish_extend(h, tokens + (n - computed), computed, base);
+  float ms = 0.f;
+  if (computed) cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->stats.gpu_ms += ms;
+  if (gpu_ms) *gpu_ms = ms;
+  if (computed_out) *computed_out = computed;
+  if (argmax_out) std::memcpy(argmax_out, h->argmax_host.data() + row_from, sizeof(int) * (n - row_from));
+  return PS_OK;
+}
+
+int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
+  if (!h || !out || first < 0 || n <= 0 || first + n > int(h->resident.size()))
+    return fail(PS_ERR_INVALID, "logits rows outside the resident sequence");
+  CK(cudaSetDevice(h->cfg.device));
+  if (!h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
+  for (int done = 0; done < n;) {
+    const int rows = std::min(kMaxWindow, n - done);
+    int slot;
+    PassCtx* hc = next_ctx_slot(h, &slot);
+    *hc = PassCtx{first + done, rows, 0, 0, 0, {0, 0, 0}};
+    CK(cudaMemcpyAsync(h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+    if (h->bf16) {
+      const ActDescs* ad = act_descs(h, round_up(rows, 16));
+      if (!ad) return fail(PS_ERR_CUDA, "TMA descriptor encode failed");
+      launch_lmhead_tc(h->d_ctx_aux, &h->tm_head, &ad->hn, h->lm_bias, h->v_begin, h->v_count, h->H,
+                       round_up(rows, 16), 0, h->am_val, h->am_idx, h->logits_buf, h->v_count, h->st);
+    } else {
+      launch_lmhead_f32(h->d_ctx_aux, rows, static_cast<const float*>(h->hn_cache), 0,
+                        static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
+                        h->am_idx, h->logits_buf, h->v_count, h->st);
+    }
+    CK(cudaMemcpyAsync(out + size_t(done) * h->v_count, h->logits_buf, sizeof(float) * size_t(rows) * h->v_count,
+                       cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    done += rows;
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand, int32_t n_cand,
+                     int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out, float* gpu_ms) {
+  if (!h || !prompt || n_prompt <= 0 || n_cand < 0 || (n_cand > 0 && !cand))
+    return fail(PS_ERR_INVALID, "verification requires a nonempty prompt context");
+  CK(cudaSetDevice(h->cfg.device));
+  std::vector<int> seq(prompt, prompt + n_prompt);
+  if (n_cand) seq.insert(seq.end(), cand, cand + n_cand);
+  const int n = int(seq.size());
+  int computed = 0, base = 0;
+  bool enq = false;
+  CK(cudaEventRecord(h->ev0, h->st));
+  if (int rc = sync_to(h, seq.data(), n, &computed, &base, &enq, false)) return rc;
+  if (n_cand) {
+    int slot;
+    next_ctx_slot(h, &slot);
+    int* ht = h->h_tok + size_t(slot) * kMaxWindow;
+    // candidate may exceed one ring slot: copy through the pinned argmax mirror tail instead
+    const int* src = cand;
+    if (n_cand <= kMaxWindow) {
+      std::memcpy(ht, cand, sizeof(int) * n_cand);
+      src = ht;
+    }
+    CK(cudaMemcpyAsync(h->d_cand, src, sizeof(int) * n_cand, cudaMemcpyHostToDevice, h->st));
+    launch_verify_compare(h->argmax_pos, n_prompt, h->d_cand, n_cand, h->term_mask, h->d_res, h->st);
+    CK(cudaMemcpyAsync(h->h_res, h->d_res, sizeof(int) * 2, cudaMemcpyDeviceToHost, h->st));
+  }
+  CK(cudaEventRecord(h->ev1, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaGetLastError());
+  if (enq) finish_extend(h, seq.data() + (n - computed), computed, base);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->stats.gpu_ms += ms;
+  const int k = n_cand ? h->h_res[0] : 0;
+  const int first_term = n_cand ? h->h_res[1] : -1;
+  if (argmax_out) std::memcpy(argmax_out, h->argmax_host.data() + (n_prompt - 1), sizeof(int) * (n_cand + 1));
+  truncate_to(h, n_prompt + k);  // KV rollback to the accepted prefix
+  if (k_out) *k_out = k;
+  if (first_term_out) *first_term_out = first_term;
+  if (gpu_ms) *gpu_ms = ms;
+  return PS_OK;
+}
+
+int ps_decode_greedy(ps_handle* h, const int32_t* seq, int32_t n_seq, int32_t max_tokens, int32_t stop_at_eos,
+                     int32_t* tokens_out, int32_t* n_out, float* token_ms) {
+  if (!h || !seq || n_seq <= 0 || max_tokens <= 0 || !tokens_out || !n_out)
+    return fail(PS_ERR_INVALID, "bad decode arguments");
+  CK(cudaSetDevice(h->cfg.device));
+  int computed = 0, base = 0;
+  bool enq = false;
+  CK(cudaEventRecord(h->ev0, h->st));
+  if (int rc = sync_to(h, seq, n_seq, &computed, &base, &enq, true)) return rc;
+  CK(cudaEventRecord(h->ev1, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaGetLastError());
+  float first_ms = 0.f;
+  if (enq) {
+    finish_extend(h, seq + (n_seq - computed), computed, base);
+    cudaEventElapsedTime(&first_ms, h->ev0, h->ev1);
+    h->stats.gpu_ms += first_ms;
+  }
+  int produced = 0;
+  tokens_out[produced] = h->argmax_host[n_seq - 1];
+  if (token_ms) token_ms[produced] = first_ms;
+  produced = 1;
+  bool stopped = stop_at_eos && tokens_out[0] == kEos;
+  std::vector<float> ms(kMaxSteps);
+  while (!stopped && produced < max_tokens) {
+    const int n0 = int(h->resident.size());
+    const int steps = std::min(kMaxSteps, max_tokens - produced);
+    int executed = 0;
+    if (int rc = run_decode_steps(h, n0, steps, stop_at_eos, &executed, ms.data())) return rc;
+    // step i processed token (previous argmax) at position n0+i and produced argmax_pos[n0+i]
+    for (int i = 0; i < executed; ++i) {
+      h->resident.push_back(h->h_steps_tok[i]);
+      h->argmax_host.push_back(h->h_argmax[n0 + i]);
+      tokens_out[produced] = h->h_argmax[n0 + i];
+      if (token_ms) token_ms[produced] = ms[i];
+      ++produced;
+      if (stop_at_eos && tokens_out[produced - 1] == kEos) {
+        stopped = true;
+        break;
+      }
+    }
+    h->stats.kv_tokens = int64_t(h->resident.size());
+    if (executed < steps) stopped = true;
+  }
+  // pages mapped for steps that never ran are released
+  {
+    const int keep = (int(h->resident.size()) + kPage - 1) / kPage;
+    while (h->pages_mapped > keep) h->free_pages.push_back(h->h_page_table[--h->pages_mapped]);
+  }
+  *n_out = produced;
+  return PS_OK;
+}
+
+int ps_truncate(ps_handle* h, int32_t n) {
+  if (!h || n < 0) return fail(PS_ERR_INVALID, "bad truncate length");
+  truncate_to(h, n);
+  return PS_OK;
+}
+
+int ps_resident(ps_handle* h, int32_t* out, int32_t cap, int32_t* n) {
+  if (!h || !n) return fail(PS_ERR_INVALID, "null argument");
+  *n = int(h->resident.size());
+  if (out) std::memcpy(out, h->resident.data(), sizeof(int) * std::min<size_t>(cap, h->resident.size()));
+  return PS_OK;
+}
+
+int ps_argmax_rows(ps_handle* h, int32_t first, int32_t n, int32_t* out) {
+  if (!h || !out || first < 0 || n < 0 || first + n > int(h->argmax_host.size()))
+    return fail(PS_ERR_INVALID, "rows outside the resident sequence");
+  std::memcpy(out, h->argmax_host.data() + first, sizeof(int) * n);
+  return PS_OK;
+}
+
+int ps_set_terminators(ps_handle* h, const uint8_t* mask, int32_t vocab) {
+  if (!h || !mask || vocab != h->V) return fail(PS_ERR_INVALID, "terminator mask must cover the vocabulary");
+  CK(cudaSetDevice(h->cfg.device));
+  CK(cudaMemcpy(h->term_mask, mask, vocab, cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+int ps_read_weights(ps_handle* h, int32_t tid, int64_t offset, int64_t count, float* out) {
+  if (!h || !out || offset < 0 || count < 0) return fail(PS_ERR_INVALID, "bad arguments");
+  CK(cudaSetDevice(h->cfg.device));
+  for (const WEntry& e : h->wreg) {
+    if (e.tid != tid) continue;
+    if (offset + count > e.count) return fail(PS_ERR_INVALID, "range outside tensor");
+    if (h->bf16) {
+      std::vector<uint16_t> tmp(count);
+      CK(cudaMemcpy(tmp.data(), static_cast<uint16_t*>(e.ptr) + offset, 2 * count, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < count; ++i) {
+        uint32_t b = uint32_t(tmp[i]) << 16;
+        std::memcpy(out + i, &b, 4);
+      }
+    } else {
+      CK(cudaMemcpy(out, static_cast<float*>(e.ptr) + offset, 4 * count, cudaMemcpyDeviceToHost));
+    }
+    return PS_OK;
+  }
+  return fail(PS_ERR_INVALID, "unknown tensor id");
+}
+
+int ps_get_stats(ps_handle* h, ps_stats* out) {
+  if (!h || !out) return fail(PS_ERR_INVALID, "null argument");
+  *out = h->stats;
+  out->kv_tokens = int64_t(h->resident.size());
+  return PS_OK;
+}
+
+int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes_out) {
+  if (!h || steps <= 0 || !ms_out) return fail(PS_ERR_INVALID, "bad arguments");
+  if (h->resident.empty()) return fail(PS_ERR_INVALID, "profile needs a resident context");
+  CK(cudaSetDevice(h->cfg.device));
+  const int n0 = int(h->resident.size());
+  if (n0 + steps > h->cfg.max_seq) return fail(PS_ERR_CAPACITY, "profile exceeds KV capacity");
+  if (int rc = map_pages(h, n0 + steps)) return rc;
+  if (!h->prof) {
+    h->prof = new Prof();
+    for (auto& e : h->prof->ev) cudaEventCreate(&e);
+  }
+  for (int c = 0; c < kProfClasses; ++c) ms_out[c] = 0.0;
+  int slot;
+  PassCtx* hc = next_ctx_slot(h, &slot);
+  *hc = PassCtx{n0, 1, 0, 0, 0, {0, 0, 0}};
+  CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+  h->prof_on = true;
+  for (int s = 0; s < steps; ++s) {
+    h->prof->n = 0;
+    enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1);
+    launch_advance(h->d_ctx, h->st);
+    cudaError_t e = cudaStreamSynchronize(h->st);
+    if (e != cudaSuccess) {
+      h->prof_on = false;
+      return fail(PS_ERR_CUDA, std::string("profile step: ") + cudaGetErrorString(e));
+    }
+    for (int i = 0; i + 1 < h->prof->n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, h->prof->ev[i], h->prof->ev[i + 1]);
+      ms_out[h->prof->cls[i]] += ms;
+    }
+  }
+  h->prof_on = false;
+  // the profiled steps only wrote positions >= n0: release their pages
+  {
+    const int keepp = (n0 + kPage - 1) / kPage;
+    while (h->pages_mapped > keepp) h->free_pages.push_back(h->h_page_table[--h->pages_mapped]);
+  }
+  for (int c = 0; c < kProfClasses; ++c) ms_out[c] /= steps;
+  if (bytes_out) {
+    const double e = double(h->esz), H = h->H, qd = h->qd, kvd = h->kvd, I = h->I, Ld = h->L;
+    const double ctx = n0 + steps / 2.0;
+    bytes_out[0] = Ld * 2 * H * 4 * 3;                     // residual streams (approx.)
+    bytes_out[1] = Ld * (qd + 2 * kvd) * H * e;            // qkv weights
+    bytes_out[2] = Ld * 2 * kvd * ctx * e;                 // KV read
+    bytes_out[3] = Ld * H * qd * e;                        // o weights
+    bytes_out[4] = Ld * 2 * I * H * e;                     // gate/up weights
+    bytes_out[5] = Ld * H * I * e;                         // down weights
+    bytes_out[6] = double(h->v_count) * H * e;             // LM head weights
+    bytes_out[7] = 0;
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_shard_init(ps_handle* h, const void* id, int32_t rank, int32_t world) {
+  (void)h;
+  (void)id;
+  (void)rank;
+  (void)world;
+  return fail(PS_ERR_UNSUPPORTED, "vocab sharding not built into this library");
+}
+
+}  // extern "C"

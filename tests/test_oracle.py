@@ -1,0 +1,77 @@
+"""The CPU oracle itself: weight generator spec, decoder contract, and the
+reference's algorithm layer replayed through this package's loop on the
+oracle decoder (config c1 golden logs, tests/golden/tiny_turns.json)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import weights as W
+from oracle.decoder import CpuDecoderLM, DecoderOracle
+from paper_2506_15556_b200 import PipelineConfig, make_stream, run_baseline, run_turn
+from paper_2506_15556_b200.model_api import LatencyModel, PrefixViolationError as PkgPrefix
+from paper_2506_15556_b200.shapes import TINY, small_shape
+from paper_2506_15556_b200.vocab import SyntheticVocabulary
+
+TINY_TURNS = json.loads((GOLDEN / "tiny_turns.json").read_text())
+
+
+def test_weight_generator_spec():
+    a = W.uniform_f32(0, 5, 1000)
+    b = W.uniform_f32(0, 5, 1000, chunk=37)
+    assert np.array_equal(a, b)
+    assert abs(a.std() - 0.02) < 0.002 and abs(a.mean()) < 0.003
+    assert np.abs(a).max() <= 0.02 * np.sqrt(3) + 1e-6
+    assert not np.array_equal(a, W.uniform_f32(1, 5, 1000))
+    assert not np.array_equal(a, W.uniform_f32(0, 6, 1000))
+    # values are k * scale with integer k: fp32-exact spec
+    k = np.round(a / W.scale_f32(0.02)).astype(np.float32)
+    assert np.array_equal(k * W.scale_f32(0.02), a)
+
+
+def test_bf16_rounding_rne():
+    x = np.array([1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -9, -2.5e-3], dtype=np.float32)
+    r = W.round_bf16(x)
+    assert r[0] == 1.0 and r[1] == 1.0  # tie to even
+    assert r[2] == 1.0 + 2 ** -7
+    assert abs(r[3] + 2.5e-3) < 2.5e-3 * 2 ** -8
+
+
+def test_decoder_cache_transparency_and_causality():
+    shape = small_shape(mode=0).as_dict()
+    m = DecoderOracle(shape, seed=3)
+    toks = [int(t) for t in np.random.default_rng(0).integers(4, 2048, 20)]
+    _, full = m.extend(toks)
+    m.reset()
+    _, a = m.extend(toks[:7])
+    _, b = m.extend(toks[7:])
+    np.testing.assert_allclose(np.concatenate([a, b]), full, rtol=1e-12, atol=1e-12)
+
+
+def test_cpu_lm_contract():
+    vocab = SyntheticVocabulary(TINY.vocab)
+    lm = CpuDecoderLM(TINY.as_dict(), vocab, seed=0)
+    ctx = [5, 6, 7, 8]
+    block, handle, cost = lm.forward(ctx)
+    assert block.rows.shape == (4, TINY.vocab) and cost == LatencyModel().pass_cost(4)
+    block2, h2, cost2 = lm.forward(ctx + [9], handle)
+    assert block2.first_position == 4 and cost2 == LatencyModel().pass_cost(1)
+    np.testing.assert_array_equal(block2.rows[0], lm.forward(ctx + [9])[0].rows[4])
+    with pytest.raises(ValueError):
+        lm.forward(ctx, h2.truncated(4))
+
+
+@pytest.mark.parametrize("i", range(len(TINY_TURNS["turns"])))
+def test_tiny_turn_replay_matches_reference(i):
+    """Reference algorithm + oracle decoder (golden) == package algorithm + oracle decoder."""
+    rec = TINY_TURNS["turns"][i]
+    vocab = SyntheticVocabulary(TINY.vocab)
+    cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
+    for arm, run in (("speculative", run_turn), ("baseline", run_baseline)):
+        lm = CpuDecoderLM(TINY_TURNS["shape"], vocab, seed=TINY_TURNS["seed"], latency=LatencyModel())
+        res = run([], make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+        assert res.final_text == rec[arm]["final_text"]
+        assert [e.to_dict() for e in res.events] == rec[arm]["events"]
+    assert rec["speculative"]["final_text"] == rec["baseline"]["final_text"]  # lossless
