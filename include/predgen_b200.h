@@ -59,6 +59,9 @@ typedef struct ps_stats {
   int64_t kv_tokens;       /* resident tokens                                      */
   int64_t kv_pages_used;
   int64_t rollbacks;       /* truncations of the resident sequence (KV rollback)  */
+  int64_t launches;        /* kernels launched by this handle (graph nodes counted per replay) */
+  int64_t h2d_bytes;       /* host->device bytes copied by API calls               */
+  int64_t d2h_bytes;       /* device->host bytes copied by API calls               */
   double weight_bytes;     /* weights streamed by one full pass                    */
   double gpu_ms;           /* accumulated measured device time                     */
 } ps_stats;

@@ -50,7 +50,8 @@ class PsStats(ctypes.Structure):
     _fields_ = [
         ("passes", ctypes.c_int64), ("rows", ctypes.c_int64), ("decode_steps", ctypes.c_int64),
         ("prefix_hits", ctypes.c_int64), ("kv_tokens", ctypes.c_int64), ("kv_pages_used", ctypes.c_int64),
-        ("rollbacks", ctypes.c_int64), ("weight_bytes", ctypes.c_double), ("gpu_ms", ctypes.c_double),
+        ("rollbacks", ctypes.c_int64), ("launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64), ("weight_bytes", ctypes.c_double), ("gpu_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -183,6 +183,12 @@ void* offset_ptr(ps_handle* h, void* base, size_t elems) {
   return static_cast<unsigned char*>(base) + elems * h->esz;
 }
 
+cudaError_t copy_async(ps_handle* h, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (kind == cudaMemcpyHostToDevice) h->stats.h2d_bytes += int64_t(bytes);
+  if (kind == cudaMemcpyDeviceToHost) h->stats.d2h_bytes += int64_t(bytes);
+  return cudaMemcpyAsync(dst, src, bytes, kind, h->st);
+}
+
 int map_pages(ps_handle* h, int n_tokens) {
   const int need = (n_tokens + kPage - 1) / kPage;
   if (need > h->g.pages) return fail(PS_ERR_CAPACITY, "context exceeds KV capacity (max_seq)");
@@ -193,8 +199,8 @@ int map_pages(ps_handle* h, int n_tokens) {
     h->h_page_table[h->pages_mapped++] = phys;
   }
   if (need > first_new) {
-    CK(cudaMemcpyAsync(h->d_page_table + first_new, h->h_page_table + first_new, sizeof(int) * (need - first_new),
-                       cudaMemcpyHostToDevice, h->st));
+    CK(copy_async(h, h->d_page_table + first_new, h->h_page_table + first_new, sizeof(int) * (need - first_new),
+                  cudaMemcpyHostToDevice));
   }
   h->stats.kv_pages_used = h->pages_mapped;
   return PS_OK;
@@ -289,7 +295,10 @@ void enqueue_pass(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, i
   prof_mark(h, 7);
 }
 
+int launches_per_pass(const ps_handle* h) { return 1 + 10 * h->L + 2; }
+
 void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
+  h->stats.launches += launches_per_pass(h);
   if (h->bf16)
     enqueue_pass<__nv_bfloat16>(h, ctx, max_rows, tok_in, max_pos);
   else
@@ -316,15 +325,15 @@ int enqueue_extend(ps_handle* h, const int* tokens, int n, int* base_out) {
     *hc = PassCtx{base + done, rows, 0, 0, 0, {0, 0, 0}};
     int* ht = h->h_tok + size_t(slot) * kMaxWindow;
     std::memcpy(ht, tokens + done, sizeof(int) * rows);
-    CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
-    CK(cudaMemcpyAsync(h->d_tok, ht, sizeof(int) * rows, cudaMemcpyHostToDevice, h->st));
+    CK(copy_async(h, h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
+    CK(copy_async(h, h->d_tok, ht, sizeof(int) * rows, cudaMemcpyHostToDevice));
     enqueue_pass_any(h, h->d_ctx, rows, h->d_tok, base + done + rows - 1);
     CK(cudaGetLastError());
     h->stats.passes += 1;
     h->stats.rows += rows;
     done += rows;
   }
-  CK(cudaMemcpyAsync(h->h_argmax + base, h->argmax_pos + base, sizeof(int) * n, cudaMemcpyDeviceToHost, h->st));
+  CK(copy_async(h, h->h_argmax + base, h->argmax_pos + base, sizeof(int) * n, cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 
@@ -366,6 +375,7 @@ int capture_decode_graph(ps_handle* h) {
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1);
   launch_advance(h->d_ctx, h->st);
+  h->stats.launches -= launches_per_pass(h);  // capture is not a launch; replays are counted
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
   if (e != cudaSuccess) return fail(PS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(e));
@@ -382,7 +392,7 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   int slot;
   PassCtx* hc = next_ctx_slot(h, &slot);
   *hc = PassCtx{n0, 1, 0, stop_at_eos, 0, {0, 0, 0}};
-  CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+  CK(copy_async(h, h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
   if (h->cfg.use_graphs) {
     if (int rc = capture_decode_graph(h)) return rc;
   }
@@ -395,7 +405,9 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   for (int i = 0; i < steps; ++i) {
     if (h->graph) {
       CK(cudaGraphLaunch(h->graph, h->st));
+      h->stats.launches += launches_per_pass(h) + 1;
     } else {
+      h->stats.launches += 1;
       enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1);
       launch_advance(h->d_ctx, h->st);
     }
@@ -403,9 +415,9 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   }
   int s2;
   PassCtx* back = next_ctx_slot(h, &s2);
-  CK(cudaMemcpyAsync(back, h->d_ctx, sizeof(PassCtx), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaMemcpyAsync(h->h_argmax + n0, h->argmax_pos + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaMemcpyAsync(h->h_steps_tok, h->tokens_dev + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost, h->st));
+  CK(copy_async(h, back, h->d_ctx, sizeof(PassCtx), cudaMemcpyDeviceToHost));
+  CK(copy_async(h, h->h_argmax + n0, h->argmax_pos + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost));
+  CK(copy_async(h, h->h_steps_tok, h->tokens_dev + n0, sizeof(int) * steps, cudaMemcpyDeviceToHost));
   CK(cudaStreamSynchronize(h->st));
   CK(cudaGetLastError());
   *executed = back->step;
@@ -639,7 +651,7 @@ int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
     int slot;
     PassCtx* hc = next_ctx_slot(h, &slot);
     *hc = PassCtx{first + done, rows, 0, 0, 0, {0, 0, 0}};
-    CK(cudaMemcpyAsync(h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+    CK(copy_async(h, h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
     if (h->bf16) {
       const ActDescs* ad = act_descs(h, round_up(rows, 16));
       if (!ad) return fail(PS_ERR_CUDA, "TMA descriptor encode failed");
@@ -650,8 +662,8 @@ int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
                         static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
                         h->am_idx, h->logits_buf, h->v_count, h->st);
     }
-    CK(cudaMemcpyAsync(out + size_t(done) * h->v_count, h->logits_buf, sizeof(float) * size_t(rows) * h->v_count,
-                       cudaMemcpyDeviceToHost, h->st));
+    CK(copy_async(h, out + size_t(done) * h->v_count, h->logits_buf, sizeof(float) * size_t(rows) * h->v_count,
+                  cudaMemcpyDeviceToHost));
     CK(cudaStreamSynchronize(h->st));
     done += rows;
   }
@@ -681,9 +693,10 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
       std::memcpy(ht, cand, sizeof(int) * n_cand);
       src = ht;
     }
-    CK(cudaMemcpyAsync(h->d_cand, src, sizeof(int) * n_cand, cudaMemcpyHostToDevice, h->st));
+    CK(copy_async(h, h->d_cand, src, sizeof(int) * n_cand, cudaMemcpyHostToDevice));
     launch_verify_compare(h->argmax_pos, n_prompt, h->d_cand, n_cand, h->term_mask, h->d_res, h->st);
-    CK(cudaMemcpyAsync(h->h_res, h->d_res, sizeof(int) * 2, cudaMemcpyDeviceToHost, h->st));
+    h->stats.launches += 1;
+    CK(copy_async(h, h->h_res, h->d_res, sizeof(int) * 2, cudaMemcpyDeviceToHost));
   }
   CK(cudaEventRecord(h->ev1, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -825,7 +838,7 @@ int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes
   int slot;
   PassCtx* hc = next_ctx_slot(h, &slot);
   *hc = PassCtx{n0, 1, 0, 0, 0, {0, 0, 0}};
-  CK(cudaMemcpyAsync(h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice, h->st));
+  CK(copy_async(h, h->d_ctx, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
   h->prof_on = true;
   for (int s = 0; s < steps; ++s) {
     h->prof->n = 0;

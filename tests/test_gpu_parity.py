@@ -1,0 +1,215 @@
+"""CUDA path vs the CPU oracle, through the C-ABI (run with -m gpu on a B200).
+
+Tolerances (stated per north_star): fp32 mode logits within rtol 1e-4 /
+atol 2e-4 of the float64 oracle, argmax ids / accept lengths / event logs
+exact; bf16 mode logits within atol 0.06 of the bf16-emulating oracle and an
+argmax agreement rate >= 97% on rows whose oracle top-2 gap exceeds 0.02.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import weights as W
+from oracle.decoder import CpuDecoderLM, DecoderOracle, top2_gap
+from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_baseline, run_turn
+from paper_2506_15556_b200.model_api import LatencyModel, PrefixViolationError, greedy_decode
+from paper_2506_15556_b200.shapes import MODE_BF16, MODE_F32, TINY, small_shape
+from paper_2506_15556_b200.vocab import SyntheticVocabulary
+
+pytestmark = pytest.mark.gpu
+
+TINY_TURNS = json.loads((GOLDEN / "tiny_turns.json").read_text())
+SMALL_BF16 = small_shape()
+SMALL_F32 = small_shape("small-f32", mode=MODE_F32)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    lm = B200LM(TINY, seed=0, max_seq=1024)
+    yield lm
+    lm.close()
+
+
+@pytest.fixture(scope="module")
+def small_bf16():
+    lm = B200LM(SMALL_BF16, seed=1, max_seq=1024)
+    yield lm
+    lm.close()
+
+
+def rand_tokens(rng, vocab, n):
+    return [int(t) for t in rng.integers(4, vocab, size=n)]
+
+
+@pytest.mark.parametrize("shape", [TINY, SMALL_BF16], ids=["f32", "bf16"])
+def test_device_weights_bit_identical_to_oracle(shape):
+    lm = B200LM(shape, seed=7, max_seq=256)
+    try:
+        bf16 = shape.mode == MODE_BF16
+        for tid, count in ((W.TID_EMBED, shape.vocab * shape.hidden), (W.TID_LM_HEAD, 4096),
+                           (W.layer_tid(0, W.WQ), 4096), (W.layer_tid(1, W.WDOWN), shape.hidden * shape.intermediate)):
+            got = lm.read_weights(tid, 0, count)
+            want = W.uniform_f32(7, tid, count)
+            if bf16:
+                want = W.bf16_bits_to_f32(W.f32_to_bf16_bits(want))
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), tid
+    finally:
+        lm.close()
+
+
+def test_f32_logits_match_oracle(tiny):
+    rng = np.random.default_rng(0)
+    toks = rand_tokens(rng, TINY.vocab, 90)
+    block, _, _ = tiny.forward(toks)
+    got = np.stack([np.asarray(block.row_for(p)) for p in range(len(toks))])
+    ref = DecoderOracle(TINY.as_dict(), seed=0)
+    _, want = ref.extend(toks)
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=2e-4)
+    gaps = np.array([top2_gap(r) for r in want])
+    ok = gaps > 1e-4
+    assert (got.argmax(1)[ok] == want.argmax(1)[ok]).all()
+    # lazy rows: np.argmax answered by the device argmax equals the materialised row's
+    assert [int(np.argmax(block.row_for(p))) for p in range(len(toks))] == list(got.argmax(1))
+
+
+def test_f32_verify_golden(tiny):
+    g = np.load(GOLDEN / "tiny_verify.npz")
+    P, R = json.loads(str(g["prompts"])), json.loads(str(g["cands"]))
+    AM, LG = json.loads(str(g["argmax"])), json.loads(str(g["logits64"]))
+    for i, (p, r) in enumerate(zip(P, R)):
+        d = tiny.verify_greedy_detail(p, r)
+        assert d["k"] == int(g["k"][i]), i
+        assert d["argmax"] == AM[i], i
+        first = next((j for j, t in enumerate(r) if t in (1, 2, 3)), -1)
+        assert d["first_term"] == first
+        assert bool(first >= 0 and d["k"] > first) == bool(g["first_sentence"][i])
+        rows = np.stack([np.asarray(tiny.forward(p + r)[0].row_for(len(p) - 1 + j))[:64] for j in range(len(r) + 1)])
+        np.testing.assert_allclose(rows, np.array(LG[i]), rtol=1e-4, atol=2e-4)
+
+
+@pytest.mark.parametrize("i", range(len(TINY_TURNS["turns"])))
+def test_f32_turn_event_logs_match_reference_golden(tiny, i):
+    rec = TINY_TURNS["turns"][i]
+    cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
+    for arm, run in (("speculative", run_turn), ("baseline", run_baseline)):
+        res = run([], make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words), cfg, tiny)
+        assert res.final_text == rec[arm]["final_text"]
+        assert [e.to_dict() for e in res.events] == rec[arm]["events"]
+
+
+def _rows_one_pass_vs_stepwise(lm, toks):
+    lm.discard_after(0)
+    block, _, _ = lm.forward(toks)
+    one = np.stack([np.asarray(block.row_for(p)) for p in range(len(toks))])
+    lm.discard_after(0)
+    step = []
+    for n in range(1, len(toks) + 1):
+        b, _, _ = lm.forward(toks[:n])
+        step.append(np.asarray(b.row_for(n - 1)))
+    return one, np.stack(step)
+
+
+@pytest.mark.parametrize("which", ["f32", "bf16"])
+def test_batch_invariance_bitwise(tiny, small_bf16, which):
+    """A row is bit-identical whether scored in a 72-row pass or a 1-row pass."""
+    lm = tiny if which == "f32" else small_bf16
+    toks = rand_tokens(np.random.default_rng(1), lm.vocab_size, 72)
+    one, step = _rows_one_pass_vs_stepwise(lm, toks)
+    assert np.array_equal(one.view(np.uint32), step.view(np.uint32))
+
+
+def test_decode_graph_matches_eager_and_forward(small_bf16):
+    toks = rand_tokens(np.random.default_rng(2), SMALL_BF16.vocab, 30)
+    fused = [t for t, _ in small_bf16.decode_greedy_fused(toks, 40)]
+    eager = B200LM(SMALL_BF16, seed=1, max_seq=1024, use_graphs=False)
+    try:
+        assert [t for t, _ in eager.decode_greedy_fused(toks, 40)] == fused
+    finally:
+        eager.close()
+    # generic per-pass greedy loop through forward() gives the same tokens
+    seq = greedy_decode(small_bf16, toks, max_new=len(fused), stop=None)
+    assert seq[len(toks):] == fused[: len(seq) - len(toks)]
+
+
+def test_bf16_agreement_with_oracle(small_bf16):
+    rng = np.random.default_rng(3)
+    ref = DecoderOracle(SMALL_BF16.as_dict(), seed=1)
+    agree = total = 0
+    for trial in range(4):
+        toks = rand_tokens(rng, SMALL_BF16.vocab, 64)
+        small_bf16.discard_after(0)
+        block, _, _ = small_bf16.forward(toks)
+        got = np.stack([np.asarray(block.row_for(p)) for p in range(len(toks))])
+        ref.reset()
+        _, want = ref.extend(toks)
+        assert np.abs(got - want).max() < 0.06
+        gaps = np.array([top2_gap(r) for r in want])
+        ok = gaps > 0.02
+        agree += int((got.argmax(1)[ok] == want.argmax(1)[ok]).sum())
+        total += int(ok.sum())
+    assert agree / total >= 0.97, (agree, total)
+
+
+@pytest.mark.parametrize("mode", ["modeled", "measured"])
+def test_bf16_pipeline_lossless(mode):
+    lm = B200LM(SMALL_BF16, seed=1, max_seq=1024, cost_mode=mode)
+    try:
+        rng = np.random.default_rng(4)
+        vocab = lm.vocab
+        cfg = PipelineConfig(system_prompt=" ".join(vocab.surface(i) for i in rand_tokens(rng, SMALL_BF16.vocab, 16)),
+                             chunk_words=2, max_response_tokens=48)
+        for trial in range(3):
+            text = " ".join(vocab.surface(i) for i in rand_tokens(rng, SMALL_BF16.vocab, int(rng.integers(6, 30))))
+            stream = make_stream(text, cfg.rate_chars_per_min, cfg.chunk_words)
+            a = run_turn([], stream, cfg, lm)
+            b = run_baseline([], stream, cfg, lm)
+            assert a.final_text == b.final_text
+    finally:
+        lm.close()
+
+
+def test_fused_and_generic_paths_agree():
+    """The reference-style generic loop (forward + np.argmax rows) and the fused
+    device paths produce identical event logs in modeled-cost mode."""
+
+    class Generic:
+        def __init__(self, lm):
+            self._lm = lm
+            self.vocab, self.latency, self._backend_id = lm.vocab, lm.latency, lm._backend_id
+
+        eos_id = 0
+
+        def forward(self, context, cache=None):
+            return self._lm.forward(context, cache)
+
+        def judge_consistency(self, a, b):
+            return self._lm.judge_consistency(a, b)
+
+    rec = TINY_TURNS["turns"][0]
+    cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
+    lm = B200LM(TINY, seed=0, max_seq=1024)
+    try:
+        stream = make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words)
+        fused = run_turn([], stream, cfg, lm)
+        generic = run_turn([], stream, cfg, Generic(lm))
+        assert [e.to_dict() for e in fused.events] == [e.to_dict() for e in generic.events]
+    finally:
+        lm.close()
+
+
+def test_contract_errors(tiny):
+    ctx = [5, 6, 7]
+    _, h, _ = tiny.forward(ctx)
+    with pytest.raises(PrefixViolationError):
+        tiny.forward([9, 9, 9, 9], h)
+    with pytest.raises(PrefixViolationError):
+        tiny.forward(ctx, h)
+    with pytest.raises(ValueError):
+        tiny.verify_greedy_fused([], [1, 2])
+    with pytest.raises(ValueError):
+        tiny.forward([4 + (i % 500) for i in range(1030)])  # beyond max_seq=1024 -> CapacityError (a ValueError)
+    # the backend recovers after an error
+    assert tiny.forward(ctx)[2] == LatencyModel().pass_cost(3)
