@@ -19,8 +19,10 @@ reference pins is the *contract* this class follows:
 Model (Llama/Qwen family): x = E[tok]; per layer x += Wo·attn(rope(Wq·n(x)+bq),
 rope(Wk·n(x)+bk), Wv·n(x)+bv); x += Wd·(silu(Wg·n(x)) ⊙ Wu·n(x)); logits =
 n(x)·Eout^T + bias, with n = RMSNorm (γ = 1). Accumulation is float64. In bf16
-mode the same rounding points as the GPU are applied (weights, normed inputs,
-q/k/v, attention output, SwiGLU product, final hidden) so the comparison
+mode the GPU's formulation is followed: the GEMM operand is bf16(x) (the
+un-normalised residual) and the RMSNorm scale is applied to the GEMM output,
+W·(x·rstd) = rstd·(W·x); the same rounding points as the GPU are applied
+(weights, bf16(x), q/k/v, attention output, SwiGLU product) so the comparison
 measures accumulation-order effects only.
 """
 
@@ -109,6 +111,14 @@ class DecoderOracle:
     def _r(self, x):
         return W.round_bf16(x).astype(self.dtype) if self.bf16 else x
 
+    def _operand(self, x):
+        """(GEMM operand, output scale): fp32 mode normalises first; bf16 mode
+        feeds bf16(x) and scales the product by rstd (csrc/gemm_tc.cu)."""
+        if self.bf16:
+            rstd = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + self.eps)
+            return self._r(x), rstd
+        return self._norm(x), 1.0
+
     def _norm(self, x):
         ms = np.mean(x * x, axis=-1, keepdims=True)
         return x / np.sqrt(ms + self.eps)
@@ -131,10 +141,10 @@ class DecoderOracle:
         scale = 1.0 / np.sqrt(self.hd)
         grp = self.nh // self.nkv
         for li, lay in enumerate(self.layers):
-            xn = self._r(self._norm(x))
-            q = xn @ lay["wq"].T
-            k = xn @ lay["wk"].T
-            v = xn @ lay["wv"].T
+            xn, sc_in = self._operand(x)
+            q = (xn @ lay["wq"].T) * sc_in
+            k = (xn @ lay["wk"].T) * sc_in
+            v = (xn @ lay["wv"].T) * sc_in
             if "bq" in lay:
                 q = q + lay["bq"]
                 k = k + lay["bk"]
@@ -157,14 +167,14 @@ class DecoderOracle:
                 o[:, h, :] = (p @ V[kh]) / p.sum(axis=1, keepdims=True)
             o = self._r(o.reshape(Wn, -1))
             x = x + o @ lay["wo"].T
-            xn = self._r(self._norm(x))
-            g = xn @ lay["wg"].T
-            u = xn @ lay["wu"].T
+            xn, sc_in = self._operand(x)
+            g = (xn @ lay["wg"].T) * sc_in
+            u = (xn @ lay["wu"].T) * sc_in
             a = self._r(g / (1.0 + np.exp(-g)) * u)
             x = x + a @ lay["wd"].T
         self.tokens.extend(int(t) for t in new_tokens)
-        hn = self._r(self._norm(x))
-        logits = hn @ self.head.T + self.bias
+        hn, sc_in = self._operand(x)
+        logits = (hn @ self.head.T) * sc_in + self.bias
         return hn, logits
 
     def ensure(self, context: list[int]) -> None:

@@ -17,6 +17,10 @@ template <typename T>
 void launch_init_uniform(T* out, uint64_t count, uint64_t first, uint64_t seed, uint32_t tid, double stddev,
                          cudaStream_t st);
 
+template <typename T>
+void launch_init_rows_interleaved(T* out, uint64_t rows, uint64_t cols, int blk, int off, uint64_t seed, uint32_t tid,
+                                  double stddev, cudaStream_t st);
+
 // Geometry of the paged KV pool: [layer][page][kv_head][kPage][head_dim] for K and for V.
 struct KvGeom {
   int layers, kv_heads, head_dim, pages;
@@ -81,12 +85,65 @@ struct TmaDesc {
 };
 bool encode_tma_2d_bf16(TmaDesc* out, const void* base, uint64_t inner, uint64_t outer,
                         uint32_t box_inner, uint32_t box_outer);
-// part[s][t][n] = sum X[t][k] W[n][k] over split s, tensor cores (tcgen05, TMEM accumulators)
-void launch_gemm_tc(const PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, float* part, int N,
-                    int K, int splits, int ntok, int x_row_offset_from_ctx, cudaStream_t st);
-void launch_lmhead_tc(const PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, const float* bias,
-                      int v_begin, int v_count, int hidden, int ntok, int pos_offset, float* am_val,
-                      int* am_idx, float* logits_out, int ld_logits, cudaStream_t st);
+// Fused epilogues of the tcgen05 weight-streaming GEMM. Split-K partials
+// are summed (in split order) by the last-arriving CTA of each 128-row tile,
+// which then applies the epilogue for its rows:
+//   QKV    * rstd + bias, RoPE, q -> q buffer, k/v -> paged KV
+//   SWIGLU * rstd, act = silu(gate) * up   (gate/up rows interleaved per tile)
+//   RESID  x += y; xb = bf16(x); per-tile sum of squares -> the grid's last
+//          tile writes rstd per row (the next GEMM applies it: y = rstd*W.xb)
+//   ARGMAX logits = rstd * (E.xb) + bias; per-tile (max, lowest id); the
+//          grid's last tile reduces over tiles -> argmax_pos[n0+t]
+enum TcMode : int { TC_EPI_QKV = 0, TC_EPI_SWIGLU = 1, TC_EPI_RESID = 2, TC_EPI_ARGMAX = 3 };
+struct TcEpilogue {
+  int mode = 0;
+  float* part = nullptr;             // split-K partials [split][kMaxWindow][N]
+  unsigned* tile_cnt = nullptr;      // per-tile arrival counters (self-resetting)
+  unsigned* grid_cnt = nullptr;      // grid-wide arrival counter (RESID / ARGMAX)
+  const float* rstd_in = nullptr;    // per-row rstd (QKV/SWIGLU: [t]; ARGMAX: [n0+t])
+  // QKV
+  const __nv_bfloat16* bias = nullptr;
+  const float2* rope = nullptr;
+  __nv_bfloat16* q = nullptr;
+  __nv_bfloat16* kpool = nullptr;
+  __nv_bfloat16* vpool = nullptr;
+  const int* page_table = nullptr;
+  KvGeom g{};
+  int layer = 0, q_dim = 0, kv_dim = 0;
+  // SWIGLU
+  __nv_bfloat16* act = nullptr;
+  int inter = 0;
+  // RESID
+  float* x = nullptr;
+  __nv_bfloat16* xb_out = nullptr;
+  int xb_out_pos = 0;                // 1: row index n0+t (hn_cache) instead of t
+  float* ssq_part = nullptr;         // [tile][kMaxWindow]
+  float* rstd_out = nullptr;
+  int rstd_out_pos = 0;
+  int hidden = 0;
+  float eps = 0.f;
+  // ARGMAX
+  const float* lbias = nullptr;
+  int v_begin = 0;
+  float* am_val = nullptr;
+  int* am_idx = nullptr;
+  float* logits_out = nullptr;
+  int ld_logits = 0;
+  int* argmax_pos = nullptr;
+  unsigned long long* packed_out = nullptr;
+  int advance = 0;                   // decode step: last CTA advances ctx->n0
+};
+void launch_tc(PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, int N, int K, int splits, int ntok,
+               int x_row_from_ctx, const TcEpilogue& e, cudaStream_t st, bool pdl);
+
+// bf16 decode-chain row kernels (layers_bf16.cu), PDL-launched
+void launch_embed_bf16(PassCtx* ctx, int max_rows, const int* tok_in, int* tokens_dev, const int* argmax_pos,
+                       const __nv_bfloat16* embed, float* x, __nv_bfloat16* xb, float* rstd, int hidden, float eps,
+                       cudaStream_t st, bool pdl);
+void launch_attention_bf16(PassCtx* ctx, int max_rows, int max_pos, const __nv_bfloat16* q,
+                           const __nv_bfloat16* kpool, const __nv_bfloat16* vpool, const int* page_table, KvGeom g,
+                           int layer, int heads, float* o_part, float* ml_part, unsigned* cnt,
+                           __nv_bfloat16* attn_out, cudaStream_t st, bool pdl);
 constexpr int kTileTc = 128;
 int tc_gemm_smem_bytes(int ntok);
 

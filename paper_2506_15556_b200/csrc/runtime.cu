@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -55,6 +57,8 @@ struct WEntry {
   int tid;
   void* ptr;
   int64_t count;
+  int64_t cols = 0;
+  int interleave_off = -1;  // >= 0: rows stored interleaved in 64-row blocks (gate/up)
 };
 
 constexpr int kCtxSlots = 64;
@@ -69,6 +73,20 @@ int choose_splits(int N, int K, int tile_n, int kgran, int max_ksplit) {
   while (tiles * s < 2 * 148 && K % (2 * s * kgran) == 0 && K / (2 * s) >= 512) s *= 2;
   while (max_ksplit > 0 && K / s > max_ksplit && K % (2 * s * kgran) == 0) s *= 2;
   return s;
+}
+
+// tcgen05 path: split-K so the grid fills the 148 SMs (2 CTAs each) in one
+// balanced wave; splits need not divide K (uneven k-block ranges are fixed by
+// (N, K) alone, so results stay independent of the pass width).
+int choose_splits_tc(int N, int K) {
+  // measured on B200 (tools/sweep_splits.py): one wave of <= 2 CTAs per SM;
+  // wide GEMMs (>= 148 tiles) run unsplit — their partial reduction costs more
+  // than the imbalance it removes.
+  const int tiles = (N + kTileTc - 1) / kTileTc, kb = K / 64;
+  if (tiles >= 148) return 1;
+  int s = std::min(16, (2 * 148) / tiles);
+  while (s > 1 && kb / s < 4) --s;
+  return std::max(1, s);
 }
 
 }  // namespace
@@ -128,6 +146,12 @@ struct ps_handle {
   PassCtx* d_ctx = nullptr;
   PassCtx* d_ctx_aux = nullptr;
   float* logits_buf = nullptr;
+  // bf16 chain state
+  float* rstd = nullptr;        // [kMaxWindow] rstd of the current residual rows
+  float* rstd_cache = nullptr;  // [seq_rows] rstd of the final hidden per position
+  float* ssq_part = nullptr;    // [H/128][kMaxWindow]
+  unsigned* counters = nullptr; // self-resetting arrival counters
+  unsigned* acnt = nullptr;     // attention page-merge counters [kMaxWindow][kv_heads]
 
   PassCtx* h_ctx = nullptr;   // pinned ring [kCtxSlots]
   int* h_tok = nullptr;       // pinned ring [kCtxSlots][kMaxWindow]
@@ -240,21 +264,20 @@ void prof_mark(ps_handle* h, int cls) {
 // One forward pass of the decoder body + LM head + argmax over `max_rows`
 // rows at ctx->n0 (device-side). tok_in == nullptr selects decode mode.
 template <typename T>
-void enqueue_pass(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
+void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
   cudaStream_t st = h->st;
   const int ntok = round_up(std::max(max_rows, 1), 16);
-  const ActDescs* ad = h->bf16 ? act_descs(h, ntok) : nullptr;
+  const ActDescs* ad = nullptr;
   T* xn = static_cast<T*>(h->xn);
   T* qb = static_cast<T*>(h->q);
   T* attn = static_cast<T*>(h->attn);
   T* act = static_cast<T*>(h->act);
   T* hn = static_cast<T*>(h->hn_cache);
+  (void)ntok;
   auto gemm = [&](const Gemm& gm, const void* X, const TmaDesc* tmx) {
-    if (h->bf16)
-      launch_gemm_tc(ctx, &gm.tm, tmx, h->part, gm.N, gm.K, gm.splits, ntok, 0, st);
-    else
-      launch_gemm_f32(ctx, max_rows, static_cast<const float*>(X), gm.K, static_cast<const float*>(gm.w), h->part,
-                      gm.N, gm.K, gm.splits, st);
+    (void)tmx;
+    launch_gemm_f32(ctx, max_rows, static_cast<const float*>(X), gm.K, static_cast<const float*>(gm.w), h->part,
+                    gm.N, gm.K, gm.splits, st);
   };
   prof_mark(h, 0);
   launch_embed_norm<T>(ctx, max_rows, tok_in, h->tokens_dev, h->argmax_pos, static_cast<const T*>(h->embed), h->x, xn,
@@ -285,24 +308,112 @@ void enqueue_pass(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, i
                             h->cfg.rms_eps, st);
   }
   prof_mark(h, 6);
-  if (h->bf16)
-    launch_lmhead_tc(ctx, &h->tm_head, &ad->hn, h->lm_bias, h->v_begin, h->v_count, h->H, ntok, 0, h->am_val,
-                     h->am_idx, nullptr, 0, st);
-  else
-    launch_lmhead_f32(ctx, max_rows, static_cast<const float*>(h->hn_cache), 0, static_cast<const float*>(h->head),
+  launch_lmhead_f32(ctx, max_rows, static_cast<const float*>(h->hn_cache), 0, static_cast<const float*>(h->head),
                       h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val, h->am_idx, nullptr, 0, st);
   launch_argmax_reduce(ctx, max_rows, h->am_val, h->am_idx, h->am_tiles, h->argmax_pos, nullptr, st);
   prof_mark(h, 7);
 }
 
-int launches_per_pass(const ps_handle* h) { return 1 + 10 * h->L + 2; }
+int launches_per_pass(const ps_handle* h) { return h->bf16 ? 1 + 5 * h->L + 1 : 1 + 10 * h->L + 2; }
 
-void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos) {
+
+// bf16 decode chain: 5 launches per layer, all PDL-chained (weights of the
+// next GEMM stream while the previous kernel drains).
+void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode) {
+  using bf = __nv_bfloat16;
+  cudaStream_t st = h->st;
+  const int ntok = round_up(std::max(max_rows, 1), 16);
+  const ActDescs* ad = act_descs(h, ntok);
+  bf* xb = static_cast<bf*>(h->xn);
+  unsigned* cnt_qkv = h->counters;
+  unsigned* cnt_o = h->counters + 1024;
+  unsigned* cnt_gu = h->counters + 2048;
+  unsigned* cnt_d = h->counters + 3072;
+  unsigned* gcnt = h->counters + 4096;  // [0] o, [1] down, [2] lm head
+  const bool pdl = true;
+  prof_mark(h, 0);
+  launch_embed_bf16(ctx, max_rows, tok_in, h->tokens_dev, h->argmax_pos, static_cast<const bf*>(h->embed), h->x, xb,
+                    h->rstd, h->H, h->cfg.rms_eps, st, pdl);
+  for (int l = 0; l < h->L; ++l) {
+    const Layer& ly = h->layers[l];
+    TcEpilogue e;
+    e.mode = TC_EPI_QKV;
+    e.part = h->part;
+    e.tile_cnt = cnt_qkv;
+    e.rstd_in = h->rstd;
+    e.bias = static_cast<const bf*>(ly.bqkv);
+    e.rope = h->rope;
+    e.q = static_cast<bf*>(h->q);
+    e.kpool = static_cast<bf*>(h->kpool);
+    e.vpool = static_cast<bf*>(h->vpool);
+    e.page_table = h->d_page_table;
+    e.g = h->g;
+    e.layer = l;
+    e.q_dim = h->qd;
+    e.kv_dim = h->kvd;
+    prof_mark(h, 1);
+    launch_tc(ctx, &ly.qkv.tm, &ad->xn, ly.qkv.N, ly.qkv.K, ly.qkv.splits, ntok, 0, e, st, pdl);
+    prof_mark(h, 2);
+    launch_attention_bf16(ctx, max_rows, max_pos, static_cast<const bf*>(h->q), static_cast<const bf*>(h->kpool),
+                          static_cast<const bf*>(h->vpool), h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part,
+                          h->acnt, static_cast<bf*>(h->attn), st, pdl);
+    TcEpilogue r;
+    r.mode = TC_EPI_RESID;
+    r.part = h->part;
+    r.tile_cnt = cnt_o;
+    r.grid_cnt = gcnt + 0;
+    r.x = h->x;
+    r.xb_out = xb;
+    r.ssq_part = h->ssq_part;
+    r.rstd_out = h->rstd;
+    r.hidden = h->H;
+    r.eps = h->cfg.rms_eps;
+    prof_mark(h, 3);
+    launch_tc(ctx, &ly.o.tm, &ad->attn, ly.o.N, ly.o.K, ly.o.splits, ntok, 0, r, st, pdl);
+    TcEpilogue g;
+    g.mode = TC_EPI_SWIGLU;
+    g.part = h->part;
+    g.tile_cnt = cnt_gu;
+    g.rstd_in = h->rstd;
+    g.act = static_cast<bf*>(h->act);
+    g.inter = h->I;
+    prof_mark(h, 4);
+    launch_tc(ctx, &ly.gu.tm, &ad->xn, ly.gu.N, ly.gu.K, ly.gu.splits, ntok, 0, g, st, pdl);
+    const bool last = l == h->L - 1;
+    r.tile_cnt = cnt_d;
+    r.grid_cnt = gcnt + 1;
+    r.xb_out = last ? static_cast<bf*>(h->hn_cache) : xb;
+    r.xb_out_pos = last ? 1 : 0;
+    r.rstd_out = last ? h->rstd_cache : h->rstd;
+    r.rstd_out_pos = last ? 1 : 0;
+    prof_mark(h, 5);
+    launch_tc(ctx, &ly.d.tm, &ad->act, ly.d.N, ly.d.K, ly.d.splits, ntok, 0, r, st, pdl);
+  }
+  TcEpilogue a;
+  a.mode = TC_EPI_ARGMAX;
+  a.grid_cnt = gcnt + 2;
+  a.rstd_in = h->rstd_cache;
+  a.lbias = h->lm_bias;
+  a.v_begin = h->v_begin;
+  a.am_val = h->am_val;
+  a.am_idx = h->am_idx;
+  a.argmax_pos = h->argmax_pos;
+  a.advance = decode ? 1 : 0;
+  prof_mark(h, 6);
+  launch_tc(ctx, &h->tm_head, &ad->hn, h->v_count, h->H, 1, ntok, 1, a, st, pdl);
+  prof_mark(h, 7);
+}
+
+// decode == true: 1-row step whose token is the previous row's argmax; the
+// step advances ctx->n0 on the device (bf16: inside the LM-head kernel).
+void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode = false) {
   h->stats.launches += launches_per_pass(h);
-  if (h->bf16)
-    enqueue_pass<__nv_bfloat16>(h, ctx, max_rows, tok_in, max_pos);
-  else
-    enqueue_pass<float>(h, ctx, max_rows, tok_in, max_pos);
+  if (h->bf16) {
+    enqueue_pass_bf16(h, ctx, max_rows, tok_in, max_pos, decode);
+  } else {
+    enqueue_pass_simt<float>(h, ctx, max_rows, tok_in, max_pos);
+    if (decode) launch_advance(ctx, h->st);
+  }
 }
 
 PassCtx* next_ctx_slot(ps_handle* h, int* slot) {
@@ -373,8 +484,7 @@ int sync_to(ps_handle* h, const int* tokens, int n, int* computed, int* base, bo
 int capture_decode_graph(ps_handle* h) {
   if (h->graph) return PS_OK;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1);
-  launch_advance(h->d_ctx, h->st);
+  enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1, true);
   h->stats.launches -= launches_per_pass(h);  // capture is not a launch; replays are counted
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
@@ -405,11 +515,9 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   for (int i = 0; i < steps; ++i) {
     if (h->graph) {
       CK(cudaGraphLaunch(h->graph, h->st));
-      h->stats.launches += launches_per_pass(h) + 1;
+      h->stats.launches += launches_per_pass(h);
     } else {
-      h->stats.launches += 1;
-      enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1);
-      launch_advance(h->d_ctx, h->st);
+      enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1, true);
     }
     CK(cudaEventRecord(h->step_ev[i + 1], h->st));
   }
@@ -497,6 +605,11 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     cudaMemcpy(h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
   }
   h->layers.resize(h->L);
+  // experiment hook: PS_TC_SPLITS="qkv,o,gu,d" overrides the split-K choice
+  int force_splits[4] = {0, 0, 0, 0};
+  if (const char* env = std::getenv("PS_TC_SPLITS")) std::sscanf(env, "%d,%d,%d,%d", &force_splits[0], &force_splits[1],
+                                                                 &force_splits[2], &force_splits[3]);
+  int gemm_idx = 0;
   const int tile_n = h->bf16 ? kTileTc : 16, kgran = h->bf16 ? 64 : 128, maxk = h->bf16 ? 0 : 2048;
   size_t part_elems = 0;
   for (int l = 0; l < h->L; ++l) {
@@ -504,7 +617,9 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     auto setup = [&](Gemm& gm, int N, int K) {
       gm.N = N;
       gm.K = K;
-      gm.splits = choose_splits(N, K, tile_n, kgran, maxk);
+      gm.splits = h->bf16 ? choose_splits_tc(N, K) : choose_splits(N, K, tile_n, kgran, maxk);
+      if (h->bf16 && force_splits[gemm_idx % 4] > 0) gm.splits = force_splits[gemm_idx % 4];
+      ++gemm_idx;
       gm.w = alloc_weights(h, size_t(N) * K);
       part_elems = std::max(part_elems, size_t(gm.splits) * kMaxWindow * N);
       return gm.w != nullptr;
@@ -515,8 +630,18 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd) * H), size_t(kvd) * H, 0, layer_tid(l, WK));
     init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd + kvd) * H), size_t(kvd) * H, 0, layer_tid(l, WV));
     init_tensor(h, ly.o.w, size_t(H) * qd, 0, layer_tid(l, WO));
-    init_tensor(h, ly.gu.w, size_t(I) * H, 0, layer_tid(l, WGATE));
-    init_tensor(h, offset_ptr(h, ly.gu.w, size_t(I) * H), size_t(I) * H, 0, layer_tid(l, WUP));
+    if (h->bf16) {
+      // gate/up rows interleaved in 64-row blocks so one 128-row GEMM tile
+      // holds matching gate and up features (SwiGLU in the GEMM epilogue)
+      auto* gu = static_cast<__nv_bfloat16*>(ly.gu.w);
+      launch_init_rows_interleaved(gu, I, H, 64, 0, c.seed, layer_tid(l, WGATE), 0.02, h->st);
+      launch_init_rows_interleaved(gu, I, H, 64, 64, c.seed, layer_tid(l, WUP), 0.02, h->st);
+      h->wreg.push_back({layer_tid(l, WGATE), gu, int64_t(I) * H, H, 0});
+      h->wreg.push_back({layer_tid(l, WUP), gu, int64_t(I) * H, H, 64});
+    } else {
+      init_tensor(h, ly.gu.w, size_t(I) * H, 0, layer_tid(l, WGATE));
+      init_tensor(h, offset_ptr(h, ly.gu.w, size_t(I) * H), size_t(I) * H, 0, layer_tid(l, WUP));
+    }
     init_tensor(h, ly.d.w, size_t(H) * I, 0, layer_tid(l, WDOWN));
     if (c.qkv_bias) {
       ly.bqkv = alloc_weights(h, size_t(qd + 2 * kvd));
@@ -533,6 +658,8 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       if (!ok) return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
     }
   }
+  if (h->bf16 && ((qd % kTileTc) || (kvd % kTileTc) || (I % 64) || (h->hd != 64 && h->hd != 128)))
+    return (ps_destroy(h), fail(PS_ERR_INVALID, "bf16 path needs q/kv dims multiple of 128, I multiple of 64"));
   h->weight_bytes = double(h->esz) * (double(h->L) * (double(qd + 2 * kvd) * H + double(H) * qd + 3.0 * H * I) +
                                       double(h->v_count) * H);
   h->stats.weight_bytes = h->weight_bytes;
@@ -571,6 +698,12 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->d_tok = h->dalloc<int>(kMaxWindow);
   h->d_cand = h->dalloc<int>(c.max_seq);
   h->d_res = h->dalloc<int>(4);
+  h->rstd = h->dalloc<float>(kMaxWindow);
+  h->rstd_cache = h->dalloc<float>(seq_rows);
+  h->ssq_part = h->dalloc<float>(size_t(H / kTileTc + 1) * kMaxWindow);
+  h->counters = h->dalloc<unsigned>(4096 + 64);
+  h->acnt = h->dalloc<unsigned>(size_t(kMaxWindow) * h->nkv);
+  if (!h->rstd || !h->rstd_cache || !h->ssq_part || !h->counters || !h->acnt) return bad("bf16 chain buffers");
   h->d_ctx = h->dalloc<PassCtx>(1);
   h->d_ctx_aux = h->dalloc<PassCtx>(1);
   h->h_ctx = h->halloc<PassCtx>(kCtxSlots);
@@ -655,8 +788,18 @@ int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
     if (h->bf16) {
       const ActDescs* ad = act_descs(h, round_up(rows, 16));
       if (!ad) return fail(PS_ERR_CUDA, "TMA descriptor encode failed");
-      launch_lmhead_tc(h->d_ctx_aux, &h->tm_head, &ad->hn, h->lm_bias, h->v_begin, h->v_count, h->H,
-                       round_up(rows, 16), 0, h->am_val, h->am_idx, h->logits_buf, h->v_count, h->st);
+      TcEpilogue a;
+      a.mode = TC_EPI_ARGMAX;
+      a.grid_cnt = h->counters + 4096 + 3;
+      a.rstd_in = h->rstd_cache;
+      a.lbias = h->lm_bias;
+      a.v_begin = h->v_begin;
+      a.am_val = h->am_val;
+      a.am_idx = h->am_idx;
+      a.argmax_pos = h->argmax_pos;  // rewrites the same ids it already holds
+      a.logits_out = h->logits_buf;
+      a.ld_logits = h->v_count;
+      launch_tc(h->d_ctx_aux, &h->tm_head, &ad->hn, h->v_count, h->H, 1, round_up(rows, 16), 1, a, h->st, false);
     } else {
       launch_lmhead_f32(h->d_ctx_aux, rows, static_cast<const float*>(h->hn_cache), 0,
                         static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
@@ -801,6 +944,21 @@ int ps_read_weights(ps_handle* h, int32_t tid, int64_t offset, int64_t count, fl
   for (const WEntry& e : h->wreg) {
     if (e.tid != tid) continue;
     if (offset + count > e.count) return fail(PS_ERR_INVALID, "range outside tensor");
+    if (e.interleave_off >= 0) {
+      std::vector<uint16_t> row(e.cols);
+      for (int64_t i = 0; i < count;) {
+        const int64_t src = offset + i, r = src / e.cols, c = src % e.cols;
+        const int64_t dr = (r / 64) * 128 + e.interleave_off + r % 64;
+        const int64_t take = std::min<int64_t>(count - i, e.cols - c);
+        CK(cudaMemcpy(row.data(), static_cast<uint16_t*>(e.ptr) + dr * e.cols + c, 2 * take, cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < take; ++k) {
+          uint32_t b = uint32_t(row[k]) << 16;
+          std::memcpy(out + i + k, &b, 4);
+        }
+        i += take;
+      }
+      return PS_OK;
+    }
     if (h->bf16) {
       std::vector<uint16_t> tmp(count);
       CK(cudaMemcpy(tmp.data(), static_cast<uint16_t*>(e.ptr) + offset, 2 * count, cudaMemcpyDeviceToHost));
@@ -842,8 +1000,7 @@ int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes
   h->prof_on = true;
   for (int s = 0; s < steps; ++s) {
     h->prof->n = 0;
-    enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1);
-    launch_advance(h->d_ctx, h->st);
+    enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1, true);
     cudaError_t e = cudaStreamSynchronize(h->st);
     if (e != cudaSuccess) {
       h->prof_on = false;
