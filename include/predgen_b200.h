@@ -129,9 +129,17 @@ int ps_get_stats(ps_handle* h, ps_stats* out);
  * algorithmic bytes of each class per step. */
 int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes_out);
 
-/* Vocab-sharded LM head (config c4): join an NCCL communicator; after every
- * pass the per-row (max logit, lowest id) keys are all-reduced with MAX. */
+/* Vocab-sharded LM head (config c4). Each instance holds LM-head rows
+ * [v_begin, v_begin + V/G) (cfg->vocab_shards = G, cfg->shard_rank). The
+ * per-row (max logit, lowest id) is packed as orderable_f32 << 32 |
+ * (0xFFFFFFFF - id); after ps_shard_init the keys of every pass are
+ * all-reduced with a uint64 MAX over NCCL (NVLink), which yields the global
+ * argmax with the lowest-id tie-break of lm.py:134-136. Without a
+ * communicator argmax ids stay shard-local and ps_shard_keys exposes the keys
+ * (tests merge them on the host). libnccl is dlopen'ed (PS_NCCL_LIB). */
+int ps_nccl_unique_id(void* out_128b);
 int ps_shard_init(ps_handle* h, const void* nccl_unique_id_128b, int32_t rank, int32_t world);
+int ps_shard_keys(ps_handle* h, int32_t first, int32_t n, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -128,6 +128,8 @@ class B200LM(LanguageModel):
         cfg.use_graphs = int(use_graphs)
         self.seed = seed
         self.max_seq = max_seq
+        self.vocab_shards = vocab_shards
+        self.shard_rank = shard_rank
         _native.check(self._lib, self._lib.ps_create(ctypes.byref(cfg), ctypes.byref(self._h)), "ps_create")
         mask = terminator_mask(vocab)
         buf = (ctypes.c_uint8 * len(mask)).from_buffer_copy(mask)
@@ -173,8 +175,27 @@ class B200LM(LanguageModel):
     def _cost(self, uncached: int, ms: float) -> float:
         return self.latency.pass_cost(uncached) if self.cost_mode == "modeled" else float(ms)
 
+    # -- vocab sharding (config c4) ------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _native.load()
+        buf = ctypes.create_string_buffer(128)
+        _native.check(lib, lib.ps_nccl_unique_id(buf), "ps_nccl_unique_id")
+        return buf.raw
+
+    def init_shard_comm(self, unique_id: bytes, rank: int, world: int) -> None:
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        self._call("ps_shard_init", buf, rank, world)
+
+    def shard_keys(self, first: int, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.uint64)
+        self._call("ps_shard_keys", first, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+        return out
+
     def _row_values(self, ctx: tuple, pos: int) -> np.ndarray:
         """fp32 logits of position `pos` given ctx[:pos+1] (re-established if rolled back)."""
+        if self.vocab_shards > 1:
+            raise NotImplementedError("logits rows of a vocab-sharded instance cover one shard only")
         res = self.resident()
         if len(res) <= pos or tuple(res[: pos + 1]) != tuple(ctx[: pos + 1]):
             # batch invariance makes the recomputed row bit-identical

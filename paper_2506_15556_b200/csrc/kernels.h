@@ -76,6 +76,9 @@ void launch_argmax_reduce(const PassCtx* ctx, int max_rows, const float* am_val,
 void launch_verify_compare(const int* argmax_pos, int p0, const int* cand, int n_cand,
                            const unsigned char* term_mask, int* res, cudaStream_t st);
 
+void launch_shard_unpack(PassCtx* ctx, const unsigned long long* keys, unsigned long long* keys_pos, int* argmax_pos,
+                         int merge, int advance, cudaStream_t st);
+
 // decode-step bookkeeping: advance n0 unless stopped.
 void launch_advance(PassCtx* ctx, cudaStream_t st);
 

@@ -376,6 +376,31 @@ void launch_verify_compare(const int* argmax_pos, int p0, const int* cand, int n
   verify_compare_kernel<<<1, 32, 0, st>>>(argmax_pos, p0, cand, n_cand, term_mask, res);
 }
 
+// Vocab-sharded LM head: after the packed (value, id) keys of this pass were
+// MAX-all-reduced across shards (or not, when merge == 0), store them per
+// position and decode the global argmax; in decode mode also advance n0.
+__global__ void shard_unpack_kernel(PassCtx* ctx, const unsigned long long* __restrict__ keys,
+                                    unsigned long long* __restrict__ keys_pos, int* __restrict__ argmax_pos, int merge,
+                                    int advance) {
+  if (ctx->stop) return;
+  const int rows = ctx->rows, n0 = ctx->n0;
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+    const unsigned long long k = keys[t];
+    keys_pos[n0 + t] = k;
+    if (merge) argmax_pos[n0 + t] = int(0xFFFFFFFFu - unsigned(k & 0xFFFFFFFFull));
+  }
+  __syncthreads();
+  if (advance && threadIdx.x == 0) {
+    ctx->n0 = n0 + 1;
+    ctx->step += 1;
+  }
+}
+
+void launch_shard_unpack(PassCtx* ctx, const unsigned long long* keys, unsigned long long* keys_pos, int* argmax_pos,
+                         int merge, int advance, cudaStream_t st) {
+  shard_unpack_kernel<<<1, 256, 0, st>>>(ctx, keys, keys_pos, argmax_pos, merge, advance);
+}
+
 __global__ void advance_kernel(PassCtx* ctx) {
   if (!ctx->stop) { ctx->n0 += 1; ctx->step += 1; }
 }

@@ -4,6 +4,8 @@
 // accept length out, one stream, one synchronisation at the end of each call.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -19,6 +21,51 @@
 using namespace ps;
 
 namespace {
+
+// ---- NCCL, loaded at run time (no link dependency; the process's own
+// libnccl — e.g. the one torch loaded — is preferred via PS_NCCL_LIB) ----
+struct NcclApi {
+  void* lib = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_init_rank)(void**, int, const void* /*ncclUniqueId by value, 128 B*/, int) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+struct NcclUniqueId {
+  char internal[128];
+};
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.lib ? &api : nullptr;
+  tried = true;
+  const char* cands[] = {std::getenv("PS_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    api.lib = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (api.lib) break;
+  }
+  if (!api.lib) return nullptr;
+  api.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(api.lib, "ncclGetUniqueId"));
+  api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+      dlsym(api.lib, "ncclAllReduce"));
+  api.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(api.lib, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(api.lib, "ncclGetErrorString"));
+  if (!api.get_unique_id || !api.all_reduce || !api.comm_destroy || !dlsym(api.lib, "ncclCommInitRank")) {
+    api.lib = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+
+// ncclCommInitRank takes ncclUniqueId by value: call through a typed pointer
+int nccl_comm_init(NcclApi* api, void** comm, int world, const NcclUniqueId& id, int rank) {
+  auto fn = reinterpret_cast<int (*)(void**, int, NcclUniqueId, int)>(dlsym(api->lib, "ncclCommInitRank"));
+  return fn(comm, world, id, rank);
+}
+constexpr int kNcclUint64 = 5, kNcclMax = 2;
 
 thread_local std::string g_err;
 
@@ -152,6 +199,10 @@ struct ps_handle {
   float* ssq_part = nullptr;    // [H/128][kMaxWindow]
   unsigned* counters = nullptr; // self-resetting arrival counters
   unsigned* acnt = nullptr;     // attention page-merge counters [kMaxWindow][kv_heads]
+  // vocab sharding (c4)
+  unsigned long long* keys = nullptr;      // [kMaxWindow] packed (value, id) of this pass
+  unsigned long long* keys_pos = nullptr;  // [seq_rows] per position
+  void* nccl_comm = nullptr;
 
   PassCtx* h_ctx = nullptr;   // pinned ring [kCtxSlots]
   int* h_tok = nullptr;       // pinned ring [kCtxSlots][kMaxWindow]
@@ -261,6 +312,8 @@ void prof_mark(ps_handle* h, int cls) {
   p->n++;
 }
 
+void enqueue_shard_merge(ps_handle* h, PassCtx* ctx, int max_rows, bool decode);
+
 // One forward pass of the decoder body + LM head + argmax over `max_rows`
 // rows at ctx->n0 (device-side). tok_in == nullptr selects decode mode.
 template <typename T>
@@ -310,12 +363,25 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
   prof_mark(h, 6);
   launch_lmhead_f32(ctx, max_rows, static_cast<const float*>(h->hn_cache), 0, static_cast<const float*>(h->head),
                       h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val, h->am_idx, nullptr, 0, st);
-  launch_argmax_reduce(ctx, max_rows, h->am_val, h->am_idx, h->am_tiles, h->argmax_pos, nullptr, st);
+  const bool sharded = h->cfg.vocab_shards > 1;
+  launch_argmax_reduce(ctx, max_rows, h->am_val, h->am_idx, h->am_tiles, h->argmax_pos, sharded ? h->keys : nullptr,
+                       st);
+  if (sharded) enqueue_shard_merge(h, ctx, max_rows, false);
   prof_mark(h, 7);
 }
 
 int launches_per_pass(const ps_handle* h) { return h->bf16 ? 1 + 5 * h->L + 1 : 1 + 10 * h->L + 2; }
 
+
+// (max, lowest id) across vocab shards: uint64 MAX all-reduce of the packed
+// keys over NCCL (one message of 8 B per row), then decode the global id.
+void enqueue_shard_merge(ps_handle* h, PassCtx* ctx, int max_rows, bool decode) {
+  if (h->nccl_comm) {
+    NcclApi* api = nccl_api();
+    api->all_reduce(h->keys, h->keys, size_t(max_rows), kNcclUint64, kNcclMax, h->nccl_comm, h->st);
+  }
+  launch_shard_unpack(ctx, h->keys, h->keys_pos, h->argmax_pos, h->nccl_comm ? 1 : 0, decode ? 1 : 0, h->st);
+}
 
 // bf16 decode chain: 5 launches per layer, all PDL-chained (weights of the
 // next GEMM stream while the previous kernel drains).
@@ -398,9 +464,12 @@ void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
   a.am_val = h->am_val;
   a.am_idx = h->am_idx;
   a.argmax_pos = h->argmax_pos;
-  a.advance = decode ? 1 : 0;
+  const bool sharded = h->cfg.vocab_shards > 1;
+  a.packed_out = sharded ? h->keys : nullptr;
+  a.advance = (decode && !sharded) ? 1 : 0;
   prof_mark(h, 6);
   launch_tc(ctx, &h->tm_head, &ad->hn, h->v_count, h->H, 1, ntok, 1, a, st, pdl);
+  if (sharded) enqueue_shard_merge(h, ctx, max_rows, decode);
   prof_mark(h, 7);
 }
 
@@ -704,6 +773,9 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->counters = h->dalloc<unsigned>(4096 + 64);
   h->acnt = h->dalloc<unsigned>(size_t(kMaxWindow) * h->nkv);
   if (!h->rstd || !h->rstd_cache || !h->ssq_part || !h->counters || !h->acnt) return bad("bf16 chain buffers");
+  h->keys = h->dalloc<unsigned long long>(kMaxWindow);
+  h->keys_pos = h->dalloc<unsigned long long>(seq_rows);
+  if (!h->keys || !h->keys_pos) return bad("shard keys");
   h->d_ctx = h->dalloc<PassCtx>(1);
   h->d_ctx_aux = h->dalloc<PassCtx>(1);
   h->h_ctx = h->halloc<PassCtx>(kCtxSlots);
@@ -748,6 +820,7 @@ void ps_destroy(ps_handle* h) {
   for (void* p : h->allocs) cudaFree(p);
   for (void* p : h->host_allocs) cudaFreeHost(p);
   if (h->logits_buf) cudaFree(h->logits_buf);
+  if (h->nccl_comm) nccl_api()->comm_destroy(h->nccl_comm);
   if (h->st) cudaStreamDestroy(h->st);
   delete h->prof;
   delete h;
@@ -1035,12 +1108,41 @@ int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes
   return PS_OK;
 }
 
+int ps_nccl_unique_id(void* out128) {
+  NcclApi* api = nccl_api();
+  if (!api) return fail(PS_ERR_UNSUPPORTED, "libnccl not found (set PS_NCCL_LIB)");
+  if (!out128) return fail(PS_ERR_INVALID, "null argument");
+  const int rc = api->get_unique_id(out128);
+  return rc ? fail(PS_ERR_CUDA, std::string("ncclGetUniqueId: ") + api->error_string(rc)) : PS_OK;
+}
+
 int ps_shard_init(ps_handle* h, const void* id, int32_t rank, int32_t world) {
-  (void)h;
-  (void)id;
-  (void)rank;
-  (void)world;
-  return fail(PS_ERR_UNSUPPORTED, "vocab sharding not built into this library");
+  if (!h || !id) return fail(PS_ERR_INVALID, "null argument");
+  if (world != std::max(1, h->cfg.vocab_shards) || rank != h->cfg.shard_rank)
+    return fail(PS_ERR_INVALID, "communicator does not match the configured vocab shards");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(PS_ERR_UNSUPPORTED, "libnccl not found (set PS_NCCL_LIB)");
+  CK(cudaSetDevice(h->cfg.device));
+  NcclUniqueId uid;
+  std::memcpy(uid.internal, id, sizeof(uid.internal));
+  void* comm = nullptr;
+  const int rc = nccl_comm_init(api, &comm, world, uid, rank);
+  if (rc) return fail(PS_ERR_CUDA, std::string("ncclCommInitRank: ") + api->error_string(rc));
+  if (h->graph) {  // the captured decode step must now include the all-reduce
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  h->nccl_comm = comm;
+  return PS_OK;
+}
+
+int ps_shard_keys(ps_handle* h, int32_t first, int32_t n, uint64_t* out) {
+  if (!h || !out || first < 0 || n < 0 || first + n > int(h->resident.size()))
+    return fail(PS_ERR_INVALID, "rows outside the resident sequence");
+  if (h->cfg.vocab_shards <= 1) return fail(PS_ERR_INVALID, "not a vocab-sharded instance");
+  CK(cudaSetDevice(h->cfg.device));
+  CK(cudaMemcpy(out, h->keys_pos + first, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return PS_OK;
 }
 
 }  // extern "C"
