@@ -126,6 +126,9 @@ class B200LM(LanguageModel):
         cfg.vocab_shards = vocab_shards
         cfg.shard_rank = shard_rank
         cfg.use_graphs = int(use_graphs)
+        # PS_LEGACY=1: multi-kernel PDL chain instead of the persistent megakernel (A/B runs)
+        import os
+        cfg.reserved[0] = 1 if os.environ.get("PS_LEGACY") == "1" else 0
         self.seed = seed
         self.max_seq = max_seq
         self.vocab_shards = vocab_shards
@@ -281,7 +284,8 @@ class B200LM(LanguageModel):
         ms = (ctypes.c_double * 8)()
         by = (ctypes.c_double * 8)()
         self._call("ps_profile_decode", steps, ms, by)
-        names = ["embed_norms", "qkv_gemm", "attention", "o_gemm", "gate_up_gemm", "down_gemm", "lm_head", "other"]
+        names = ["embed_norms", "qkv_gemm", "attention", "o_gemm", "gate_up_gemm", "down_gemm", "lm_head",
+                 "whole_pass"]
         return {n: {"ms": ms[i], "bytes": by[i]} for i, n in enumerate(names)}
 
     @property

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -149,5 +150,50 @@ void launch_attention_bf16(PassCtx* ctx, int max_rows, int max_pos, const __nv_b
                            __nv_bfloat16* attn_out, cudaStream_t st, bool pdl);
 constexpr int kTileTc = 128;
 int tc_gemm_smem_bytes(int ntok);
+
+// ---- persistent megakernel (megakernel.cu): one cooperative launch per pass ----
+struct MegaParams {
+  PassCtx* ctx;
+  int decode;               // 1: 1-row step, token = previous argmax
+  int advance;              // decode: last LM CTA advances ctx->n0
+  const int* tok_in;        // extend passes
+  int L, H, qd, kvd, I, hd, heads, kv_heads, vocab_local, v_begin;
+  int ntok, stages, acc_cols, max_splits_attn;
+  float eps, attn_scale;
+  const CUtensorMap* wmaps; // [4L + 1] device-resident tensor maps
+  const CUtensorMap* xmaps; // [4] activation maps for this ntok: xb, attn, act, hn
+  int* tokens_dev;
+  int* argmax_pos;
+  const __nv_bfloat16* embed;
+  const __nv_bfloat16* qkv_bias;  // [L][qd+2kvd] or null
+  const float2* rope;
+  const float* lm_bias;
+  float* x;
+  __nv_bfloat16* xb;
+  float* rstd0;
+  float* ssq_part;
+  __nv_bfloat16* q;
+  __nv_bfloat16* kpool;
+  __nv_bfloat16* vpool;
+  const int* page_table;
+  KvGeom g;
+  __nv_bfloat16* attn;
+  __nv_bfloat16* act;
+  __nv_bfloat16* hn_cache;
+  float* rstd_cache;
+  float* o_part;
+  float* ml_part;
+  unsigned* acnt;
+  float* part;              // [G][2][kMaxWindow][128] stream-K piece partials
+  unsigned* tile_cnt;
+  unsigned* lm_cnt;
+  float* am_val;
+  int* am_idx;
+  unsigned long long* keys;
+  unsigned* bar;            // grid barrier counter, zeroed before launch
+};
+int mega_stages(int ntok, int attn_floats);
+int mega_smem_bytes(int ntok, int stages, int attn_floats);
+cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st);
 
 }  // namespace ps

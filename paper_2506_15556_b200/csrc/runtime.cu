@@ -199,6 +199,15 @@ struct ps_handle {
   float* ssq_part = nullptr;    // [H/128][kMaxWindow]
   unsigned* counters = nullptr; // self-resetting arrival counters
   unsigned* acnt = nullptr;     // attention page-merge counters [kMaxWindow][kv_heads]
+  // megakernel
+  bool mega = true;
+  int sms = 148;
+  CUtensorMap* d_wmaps = nullptr;           // [4L+1]
+  CUtensorMap* d_xmaps = nullptr;           // [ntok/16][4]
+  std::vector<int> xmaps_ready;             // per ntok/16
+  __nv_bfloat16* qkv_bias_all = nullptr;
+  float* mega_part = nullptr;
+  unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [64..] tile counters
   // vocab sharding (c4)
   unsigned long long* keys = nullptr;      // [kMaxWindow] packed (value, id) of this pass
   unsigned long long* keys_pos = nullptr;  // [seq_rows] per position
@@ -370,7 +379,10 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
   prof_mark(h, 7);
 }
 
-int launches_per_pass(const ps_handle* h) { return h->bf16 ? 1 + 5 * h->L + 1 : 1 + 10 * h->L + 2; }
+int launches_per_pass(const ps_handle* h) {
+  if (h->mega) return 1 + (h->cfg.vocab_shards > 1 ? 1 : 0);
+  return h->bf16 ? 1 + 5 * h->L + 1 : 1 + 10 * h->L + 2;
+}
 
 
 // (max, lowest id) across vocab shards: uint64 MAX all-reduce of the packed
@@ -383,10 +395,71 @@ void enqueue_shard_merge(ps_handle* h, PassCtx* ctx, int max_rows, bool decode) 
   launch_shard_unpack(ctx, h->keys, h->keys_pos, h->argmax_pos, h->nccl_comm ? 1 : 0, decode ? 1 : 0, h->st);
 }
 
+// bf16 pass as ONE persistent cooperative kernel (megakernel.cu).
+void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, bool decode) {
+  using bf = __nv_bfloat16;
+  const int ntok = round_up(std::max(max_rows, 1), 16);
+  const int grp = h->nh / h->nkv;
+  const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + grp * h->hd;
+  MegaParams P{};
+  P.ctx = ctx;
+  P.decode = decode ? 1 : 0;
+  const bool sharded = h->cfg.vocab_shards > 1;
+  P.advance = (decode && !sharded) ? 1 : 0;
+  P.tok_in = tok_in;
+  P.L = h->L; P.H = h->H; P.qd = h->qd; P.kvd = h->kvd; P.I = h->I; P.hd = h->hd;
+  P.heads = h->nh; P.kv_heads = h->nkv; P.vocab_local = h->v_count; P.v_begin = h->v_begin;
+  P.ntok = ntok;
+  P.stages = mega_stages(ntok, attn_floats);
+  int cols = 32;
+  while (cols < ntok) cols <<= 1;
+  P.acc_cols = cols;
+  P.max_splits_attn = h->cfg.max_seq / kPage + 1;
+  P.eps = h->cfg.rms_eps;
+  P.attn_scale = float(1.0 / std::sqrt(double(h->hd)));
+  P.wmaps = h->d_wmaps;
+  P.xmaps = h->d_xmaps + size_t(ntok / 16 - 1) * 4;
+  P.tokens_dev = h->tokens_dev;
+  P.argmax_pos = h->argmax_pos;
+  P.embed = static_cast<const bf*>(h->embed);
+  P.qkv_bias = h->qkv_bias_all;
+  P.rope = h->rope;
+  P.lm_bias = h->lm_bias;
+  P.x = h->x;
+  P.xb = static_cast<bf*>(h->xn);
+  P.rstd0 = h->rstd;
+  P.ssq_part = h->ssq_part;
+  P.q = static_cast<bf*>(h->q);
+  P.kpool = static_cast<bf*>(h->kpool);
+  P.vpool = static_cast<bf*>(h->vpool);
+  P.page_table = h->d_page_table;
+  P.g = h->g;
+  P.attn = static_cast<bf*>(h->attn);
+  P.act = static_cast<bf*>(h->act);
+  P.hn_cache = static_cast<bf*>(h->hn_cache);
+  P.rstd_cache = h->rstd_cache;
+  P.o_part = h->o_part;
+  P.ml_part = h->ml_part;
+  P.acnt = h->acnt;
+  P.part = h->mega_part;
+  P.tile_cnt = h->mega_cnt + 64;
+  P.lm_cnt = h->mega_cnt + 1;
+  P.am_val = h->am_val;
+  P.am_idx = h->am_idx;
+  P.keys = sharded ? h->keys : nullptr;
+  P.bar = h->mega_cnt;
+  cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned), h->st);
+  prof_mark(h, 7);
+  launch_mega(P, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
+  if (sharded) enqueue_shard_merge(h, ctx, max_rows, decode);
+  prof_mark(h, 6);
+}
+
 // bf16 decode chain: 5 launches per layer, all PDL-chained (weights of the
 // next GEMM stream while the previous kernel drains).
 void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode) {
   using bf = __nv_bfloat16;
+  if (h->mega) return enqueue_mega(h, ctx, max_rows, tok_in, decode);
   cudaStream_t st = h->st;
   const int ntok = round_up(std::max(max_rows, 1), 16);
   const ActDescs* ad = act_descs(h, ntok);
@@ -674,6 +747,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     cudaMemcpy(h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
   }
   h->layers.resize(h->L);
+  if (h->bf16 && c.qkv_bias) {
+    h->qkv_bias_all = h->dalloc<__nv_bfloat16>(size_t(h->L) * (qd + 2 * kvd));
+    if (!h->qkv_bias_all) return bad("qkv bias");
+  }
   // experiment hook: PS_TC_SPLITS="qkv,o,gu,d" overrides the split-K choice
   int force_splits[4] = {0, 0, 0, 0};
   if (const char* env = std::getenv("PS_TC_SPLITS")) std::sscanf(env, "%d,%d,%d,%d", &force_splits[0], &force_splits[1],
@@ -713,7 +790,8 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     }
     init_tensor(h, ly.d.w, size_t(H) * I, 0, layer_tid(l, WDOWN));
     if (c.qkv_bias) {
-      ly.bqkv = alloc_weights(h, size_t(qd + 2 * kvd));
+      ly.bqkv = h->qkv_bias_all ? static_cast<void*>(h->qkv_bias_all + size_t(l) * (qd + 2 * kvd))
+                                : alloc_weights(h, size_t(qd + 2 * kvd));
       if (!ly.bqkv) return bad("bias");
       init_tensor(h, ly.bqkv, qd, 0, layer_tid(l, BQ));
       init_tensor(h, offset_ptr(h, ly.bqkv, qd), kvd, 0, layer_tid(l, BK));
@@ -788,6 +866,36 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       !h->d_cand || !h->d_res || !h->d_ctx || !h->d_ctx_aux || !h->h_ctx || !h->h_tok || !h->h_res ||
       !h->h_argmax || !h->h_steps_tok)
     return bad("workspace");
+  h->mega = h->bf16 && c.reserved[0] == 0;
+  if (h->mega) {
+    int dev_sms = 0;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
+    h->sms = dev_sms > 0 ? dev_sms : 148;
+    h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128);
+    h->mega_cnt = h->dalloc<unsigned>(64 + 2048);
+    h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
+    h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
+    if (!h->mega_part || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
+    std::vector<CUtensorMap> wm(size_t(4) * h->L + 1);
+    for (int l = 0; l < h->L; ++l) {
+      std::memcpy(&wm[4 * l + 0], h->layers[l].qkv.tm.bytes, sizeof(CUtensorMap));
+      std::memcpy(&wm[4 * l + 1], h->layers[l].o.tm.bytes, sizeof(CUtensorMap));
+      std::memcpy(&wm[4 * l + 2], h->layers[l].gu.tm.bytes, sizeof(CUtensorMap));
+      std::memcpy(&wm[4 * l + 3], h->layers[l].d.tm.bytes, sizeof(CUtensorMap));
+    }
+    std::memcpy(&wm[4 * h->L], h->tm_head.bytes, sizeof(CUtensorMap));
+    cudaMemcpy(h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice);
+    std::vector<CUtensorMap> xm(size_t(kMaxWindow / 16) * 4);
+    for (int k = 0; k < kMaxWindow / 16; ++k) {
+      const ActDescs* ad = act_descs(h, 16 * (k + 1));
+      if (!ad) return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
+      std::memcpy(&xm[4 * k + 0], ad->xn.bytes, sizeof(CUtensorMap));
+      std::memcpy(&xm[4 * k + 1], ad->attn.bytes, sizeof(CUtensorMap));
+      std::memcpy(&xm[4 * k + 2], ad->act.bytes, sizeof(CUtensorMap));
+      std::memcpy(&xm[4 * k + 3], ad->hn.bytes, sizeof(CUtensorMap));
+    }
+    cudaMemcpy(h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
+  }
   {
     // RoPE table (rotate-half pairs): angle = pos * theta^(-2i/hd), in fp64.
     const int half = h->hd / 2;
@@ -1103,6 +1211,12 @@ int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes
     bytes_out[5] = Ld * H * I * e;                         // down weights
     bytes_out[6] = double(h->v_count) * H * e;             // LM head weights
     bytes_out[7] = 0;
+    if (h->mega) {  // one kernel per pass: report the whole pass under "other"
+      double all = 0;
+      for (int i = 0; i < 7; ++i) all += bytes_out[i];
+      for (int i = 0; i < 7; ++i) bytes_out[i] = 0;
+      bytes_out[7] = all - Ld * 2 * H * 4 * 3 + Ld * 2 * kvd * e;  // weights + KV read + KV append
+    }
   }
   CK(cudaGetLastError());
   return PS_OK;

@@ -159,7 +159,41 @@ def make_tiny():
     print("tiny verify cases:", len(K), "k:", K)
 
 
+def make_c2(n_turns: int = 1):
+    """Config c2: Qwen2.5-0.5B shape, fp32, 128-token query in 16 chunks, cap 64."""
+    from paper_2506_15556_b200.shapes import QWEN_05B
+    shape = QWEN_05B.as_dict()
+    vocab = SyntheticVocabulary(QWEN_05B.vocab)
+    cfg = RefConfig(system_prompt="", chunk_words=8, max_response_tokens=64)
+    turns, trial = [], 0
+    lm = CpuDecoderLM(shape, vocab, seed=0, latency=ref_lm.LatencyModel())
+    while len(turns) < n_turns and trial < 6:
+        rng = np.random.default_rng(9000 + trial)
+        text = tiny_prompt(rng, vocab, 128)
+        rec = {"trial": trial, "prompt": text}
+        ok = True
+        for baseline in (False, True):
+            lm.min_gap = np.inf
+            run = ref.run_baseline if baseline else ref.run_turn
+            res = run([], ref.make_stream(text, cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+            rec["baseline" if baseline else "speculative"] = {
+                "final_text": res.final_text, "nfe_total": res.nfe_total, "events": events_json(res),
+                "min_gap": float(lm.min_gap)}
+            ok = ok and lm.min_gap > GAP_MIN
+            print("c2 trial", trial, "baseline" if baseline else "spec", "passes", lm.passes, "gap", lm.min_gap,
+                  flush=True)
+        if ok:
+            turns.append(rec)
+        trial += 1
+    (HERE / "c2_turns.json").write_text(json.dumps({"shape": shape, "config": "c2", "seed": 0, "turns": turns},
+                                                   sort_keys=True) + "\n")
+    print("c2 turns kept:", len(turns), "of", trial)
+
+
 if __name__ == "__main__":
+    if "--c2" in sys.argv:
+        make_c2()
+        sys.exit(0)
     make_ngram()
     if "--skip-decoder" not in sys.argv:
         make_tiny()
