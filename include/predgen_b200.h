@@ -129,6 +129,13 @@ int ps_get_stats(ps_handle* h, ps_stats* out);
  * algorithmic bytes of each class per step. */
 int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes_out);
 
+/* Megakernel timeline of the last pass (only when PS_TRACE=1 at ps_create):
+ * out[(phase * ctas + cta) * 8 + slot] in ns (globaltimer); slots: 0 producer
+ * passed the barrier, 1 workers passed it, 2 workers finished the phase, 3 MMA
+ * issue finished, 4 workers saw the last accumulator, 5 partials published,
+ * 6 deferred finalisation done. */
+int ps_trace(ps_handle* h, uint64_t* out, int64_t cap, int32_t* nphases, int32_t* ctas);
+
 /* Vocab-sharded LM head (config c4). Each instance holds LM-head rows
  * [v_begin, v_begin + V/G) (cfg->vocab_shards = G, cfg->shard_rank). The
  * per-row (max logit, lowest id) is packed as orderable_f32 << 32 |

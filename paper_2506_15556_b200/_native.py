@@ -82,6 +82,7 @@ SIGNATURES = {
     "ps_read_weights": (ctypes.c_int, [_h, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _f32p]),
     "ps_get_stats": (ctypes.c_int, [_h, _P(PsStats)]),
     "ps_profile_decode": (ctypes.c_int, [_h, ctypes.c_int32, _f64p, _f64p]),
+    "ps_trace": (ctypes.c_int, [_h, _P(ctypes.c_uint64), ctypes.c_int64, _i32p, _i32p]),
     "ps_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "ps_shard_init": (ctypes.c_int, [_h, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]),
     "ps_shard_keys": (ctypes.c_int, [_h, ctypes.c_int32, ctypes.c_int32, _P(ctypes.c_uint64)]),

@@ -126,9 +126,6 @@ class B200LM(LanguageModel):
         cfg.vocab_shards = vocab_shards
         cfg.shard_rank = shard_rank
         cfg.use_graphs = int(use_graphs)
-        # PS_LEGACY=1: multi-kernel PDL chain instead of the persistent megakernel (A/B runs)
-        import os
-        cfg.reserved[0] = 1 if os.environ.get("PS_LEGACY") == "1" else 0
         self.seed = seed
         self.max_seq = max_seq
         self.vocab_shards = vocab_shards

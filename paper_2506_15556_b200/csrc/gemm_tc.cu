@@ -420,6 +420,11 @@ bool encode_tma_2d_bf16(TmaDesc* out, const void* base, uint64_t inner, uint64_t
 
 void launch_tc(PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, int N, int K, int splits, int ntok,
                int x_row_from_ctx, const TcEpilogue& e, cudaStream_t st, bool pdl) {
+  // Only the LM-head ARGMAX mode is live: the decode/verify passes run in the
+  // persistent megakernel, whose weight layouts (kHeadPairs / kGateUp) the
+  // QKV / SWIGLU modes below do not follow. ps_logits_rows uses ARGMAX with
+  // logits_out for the parity path.
+  if (e.mode != TC_EPI_ARGMAX) return;
   TcParams p{};
   p.N = N;
   p.kblocks = K / kBK;

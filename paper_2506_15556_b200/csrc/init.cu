@@ -46,38 +46,38 @@ void launch_init_uniform(T* out, uint64_t count, uint64_t first, uint64_t seed, 
                                                                weight_scale(stddev));
 }
 
-// Same values, written to interleaved destination rows: source row r goes to
-// (r / blk) * 2 * blk + off + r % blk (gate/up rows sharing one 128-row tile).
+// Same values, written to permuted destination rows (row r of the tensor ->
+// perm_row(r)); the fused bf16 matrices store partner rows next to each other
+// so the GEMM epilogue exchanges them with one shuffle (see kernels.h).
 template <typename T>
-__global__ void init_rows_interleaved_kernel(T* __restrict__ out, uint64_t rows, uint64_t cols, uint64_t key,
-                                             float scale, int blk, int off) {
+__global__ void init_rows_permuted_kernel(T* __restrict__ out, uint64_t rows, uint64_t cols, uint64_t key,
+                                          float scale, RowPerm perm) {
   const uint64_t count = rows * cols;
   uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (; i < count; i += stride) {
     const uint64_t r = i / cols, c = i % cols;
-    const uint64_t dr = (r / blk) * 2 * blk + off + r % blk;
     uint64_t h = mix64(key + (i + 1) * 0x9E3779B97F4A7C15ull);
     int32_t u = int32_t(h >> 41) - (1 << 22);
-    out[dr * cols + c] = from_f32<T>(__fmul_rn(float(u), scale));
+    out[uint64_t(perm.dst(int(r))) * cols + c] = from_f32<T>(__fmul_rn(float(u), scale));
   }
 }
 
 template <typename T>
-void launch_init_rows_interleaved(T* out, uint64_t rows, uint64_t cols, int blk, int off, uint64_t seed, uint32_t tid,
-                                  double stddev, cudaStream_t st) {
+void launch_init_rows_permuted(T* out, uint64_t rows, uint64_t cols, RowPerm perm, uint64_t seed, uint32_t tid,
+                               double stddev, cudaStream_t st) {
   const uint64_t count = rows * cols;
   if (count == 0) return;
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 148ull * 64) blocks = 148ull * 64;
-  init_rows_interleaved_kernel<T><<<unsigned(blocks), 256, 0, st>>>(out, rows, cols, weight_key(seed, tid),
-                                                                   weight_scale(stddev), blk, off);
+  init_rows_permuted_kernel<T><<<unsigned(blocks), 256, 0, st>>>(out, rows, cols, weight_key(seed, tid),
+                                                                weight_scale(stddev), perm);
 }
 
-template void launch_init_rows_interleaved<__nv_bfloat16>(__nv_bfloat16*, uint64_t, uint64_t, int, int, uint64_t,
-                                                          uint32_t, double, cudaStream_t);
-template void launch_init_rows_interleaved<float>(float*, uint64_t, uint64_t, int, int, uint64_t, uint32_t, double,
-                                                  cudaStream_t);
+template void launch_init_rows_permuted<__nv_bfloat16>(__nv_bfloat16*, uint64_t, uint64_t, RowPerm, uint64_t,
+                                                       uint32_t, double, cudaStream_t);
+template void launch_init_rows_permuted<float>(float*, uint64_t, uint64_t, RowPerm, uint64_t, uint32_t, double,
+                                               cudaStream_t);
 
 template void launch_init_uniform<float>(float*, uint64_t, uint64_t, uint64_t, uint32_t, double, cudaStream_t);
 template void launch_init_uniform<__nv_bfloat16>(__nv_bfloat16*, uint64_t, uint64_t, uint64_t, uint32_t, double,

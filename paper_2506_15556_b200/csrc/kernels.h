@@ -18,9 +18,30 @@ template <typename T>
 void launch_init_uniform(T* out, uint64_t count, uint64_t first, uint64_t seed, uint32_t tid, double stddev,
                          cudaStream_t st);
 
+// Row permutations of the fused bf16 weight matrices.
+//   kHeadPairs: within each head of `hd` rows, dims i and i+hd/2 (a RoPE
+//               rotate-half pair) sit at rows 2i and 2i+1;
+//   kGateUp:    gate feature j -> row 2j, up feature j -> row 2j+1
+//               (`off` = 0 for gate, 1 for up), so a 128-row tile holds 64
+//               complete SwiGLU pairs.
+struct RowPerm {
+  enum Kind : int { kIdentity = 0, kHeadPairs = 1, kGateUp = 2 };
+  int kind = kIdentity;
+  int hd = 0;       // kHeadPairs
+  int off = 0;      // kGateUp
+  int base = 0;     // destination row offset inside the fused matrix
+  __host__ __device__ int dst(int r) const {
+    if (kind == kHeadPairs) {
+      const int h = r / hd, i = r % hd, half = hd / 2;
+      return base + h * hd + (i < half ? 2 * i : 2 * (i - half) + 1);
+    }
+    if (kind == kGateUp) return base + 2 * r + off;
+    return base + r;
+  }
+};
 template <typename T>
-void launch_init_rows_interleaved(T* out, uint64_t rows, uint64_t cols, int blk, int off, uint64_t seed, uint32_t tid,
-                                  double stddev, cudaStream_t st);
+void launch_init_rows_permuted(T* out, uint64_t rows, uint64_t cols, RowPerm perm, uint64_t seed, uint32_t tid,
+                               double stddev, cudaStream_t st);
 
 // Geometry of the paged KV pool: [layer][page][kv_head][kPage][head_dim] for K and for V.
 struct KvGeom {
@@ -140,14 +161,6 @@ struct TcEpilogue {
 void launch_tc(PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, int N, int K, int splits, int ntok,
                int x_row_from_ctx, const TcEpilogue& e, cudaStream_t st, bool pdl);
 
-// bf16 decode-chain row kernels (layers_bf16.cu), PDL-launched
-void launch_embed_bf16(PassCtx* ctx, int max_rows, const int* tok_in, int* tokens_dev, const int* argmax_pos,
-                       const __nv_bfloat16* embed, float* x, __nv_bfloat16* xb, float* rstd, int hidden, float eps,
-                       cudaStream_t st, bool pdl);
-void launch_attention_bf16(PassCtx* ctx, int max_rows, int max_pos, const __nv_bfloat16* q,
-                           const __nv_bfloat16* kpool, const __nv_bfloat16* vpool, const int* page_table, KvGeom g,
-                           int layer, int heads, float* o_part, float* ml_part, unsigned* cnt,
-                           __nv_bfloat16* attn_out, cudaStream_t st, bool pdl);
 constexpr int kTileTc = 128;
 int tc_gemm_smem_bytes(int ntok);
 
@@ -185,15 +198,18 @@ struct MegaParams {
   float* ml_part;
   unsigned* acnt;
   float* part;              // [G][2][kMaxWindow][128] stream-K piece partials
-  unsigned* tile_cnt;
+  unsigned* tile_cnt;       // [phase][max_tiles], zeroed before the pass
+  int max_tiles;
   unsigned* lm_cnt;
   float* am_val;
   int* am_idx;
   unsigned long long* keys;
   unsigned* bar;            // grid barrier counter, zeroed before launch
+  unsigned long long* trace;  // optional [nphases][G][4] globaltimer stamps
 };
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);
 cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st);
+int mega_max_blocks_per_sm(int smem);
 
 }  // namespace ps

@@ -27,7 +27,7 @@ namespace ps {
 
 namespace {
 
-enum Phase : int { PH_EMBED = 0, PH_QKV, PH_ATTN, PH_O, PH_GU, PH_D, PH_LM };
+enum Phase : int { PH_EMBED = 0, PH_QKV, PH_ATTN, PH_O, PH_GU, PH_D, PH_LM, PH_FINAL };
 constexpr int kWorkers = 128;  // warps 2..5
 
 __device__ __forceinline__ void wk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -35,6 +35,7 @@ __device__ __forceinline__ void wk_bar() { asm volatile("bar.sync 1, 128;" ::: "
 struct Gemm {
   int N, KB, T;  // rows, k-blocks per tile, total k-blocks
   int tiles;
+  int G;         // CTAs sharing this phase (<= grid): at most 8 pieces per tile
 };
 
 __device__ __forceinline__ Gemm gemm_of(const MegaParams& P, int kind) {
@@ -48,13 +49,27 @@ __device__ __forceinline__ Gemm gemm_of(const MegaParams& P, int kind) {
   }
   g.tiles = (g.N + 127) / 128;
   g.T = g.tiles * g.KB;
+  // pieces per tile <= ceil(KB / (T/G)) + 1 <= 8  <=>  G <= 7 * tiles
+  g.G = min(min(int(gridDim.x), 7 * g.tiles), g.T);  // and T >= G: no empty CTA ranges
   return g;
 }
 
-__device__ __forceinline__ int sk_start(int c, int G, int T) { return int((long long)c * T / G); }
+// (c * T fits in 32 bits: T <= 1002 tiles x 64 k-blocks, c <= 148)
+__device__ __forceinline__ int sk_start(int c, int G, int T) { return (c * T) / G; }
 // CTA whose k-block range contains global block x
-__device__ __forceinline__ int sk_owner(int x, int G, int T) {
-  return int(((long long)(x + 1) * G + T - 1) / T) - 1;
+__device__ __forceinline__ int sk_owner(int x, int G, int T) { return ((x + 1) * G + T - 1) / T - 1; }
+
+// atomic add with acquire+release at GPU scope: orders this CTA's prior
+// writes (made visible to thread 0 by the preceding bar.sync) before the
+// counter update, and the finalizer's later reads after it.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ void grid_arrive(unsigned* bar) {
@@ -62,12 +77,29 @@ __device__ __forceinline__ void grid_arrive(unsigned* bar) {
 }
 
 __device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
-  while (ld_acquire_gpu(bar) < target) __nanosleep(40);
+  while (ld_acquire_gpu(bar) < target) {
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// trace slots per (phase, CTA): 0 producer passed barrier, 1 workers passed
+// barrier, 2 workers finished the phase, 3 MMA issue finished, 4 workers saw
+// the last accumulator, 5 workers published all partials, 6 workers done with
+// the deferred finalisation
+constexpr int kTraceSlots = 12;
+__device__ __forceinline__ void stamp(const MegaParams& P, int p, int c, int G, int slot) {
+  if (P.trace) P.trace[(size_t(p) * G + c) * kTraceSlots + slot] = gtime();
 }
 
 __device__ __forceinline__ int phase_kind(int p, int L) {
   if (p == 0) return PH_EMBED;
   if (p == 1 + 5 * L) return PH_LM;
+  if (p == 2 + 5 * L) return PH_FINAL;
   return PH_QKV + (p - 1) % 5;
 }
 
@@ -85,69 +117,64 @@ __device__ __forceinline__ const CUtensorMap* xmap_of(const MegaParams& P, int k
 // ---------------------------------------------------------------------------
 // epilogue math for one finished 8-column chunk of tile rows [128*tile, +128)
 struct EpiSmem {
-  float xch[8][128];
+  float am_v[4][kMaxWindow];  // LM head: running (max, id) per warp quadrant and row
+  int am_i[4][kMaxWindow];
   float red_v[4][8];
   int red_i[4][8];
   float rstd[kMaxWindow];
   int flag;
+  int rflag[8];
 };
 
-__device__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows, int n0, int tile, int m, int q,
+// Barrier-free: every warp finishes its own 32 rows. RoPE / SwiGLU partners
+// are adjacent rows (RowPerm kHeadPairs / kGateUp) -> one shuffle; row sums
+// (sum of squares, argmax) stay per warp quadrant and are combined by their
+// consumer in a fixed order.
+__device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows, int n0, int tile, int m, int q,
                              int lane, int c0, const float (&v)[8], EpiSmem& es) {
   const int n = tile * 128 + m;
-  if (kind == PH_QKV || kind == PH_GU) {
-    float val[8];
-    const __nv_bfloat16* bias = (kind == PH_QKV && P.qkv_bias) ? P.qkv_bias + size_t(layer) * (P.qd + 2 * P.kvd) : nullptr;
+  if (kind == PH_QKV) {
+    const int hd = P.hd, half = hd >> 1;
+    const int r = n % hd, pi = r >> 1;
+    const bool even = (r & 1) == 0;
+    const int dim = even ? pi : pi + half;  // dimension within the head
+    const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
+    const float bias = P.qkv_bias ? __bfloat162float(P.qkv_bias[size_t(layer) * (P.qd + 2 * P.kvd) + n]) : 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int t = c0 + j;
-      val[j] = 0.f;
-      if (t < rows) {
-        val[j] = v[j] * es.rstd[t];
-        if (bias) val[j] += __bfloat162float(bias[n]);
+      const bool valid = t < rows;
+      const float val = valid ? v[j] * es.rstd[t] + bias : 0.f;
+      const float other = __shfl_xor_sync(0xffffffffu, val, 1);
+      if (!valid) continue;
+      const int pos = n0 + t;
+      float out = val;
+      if (is_q || is_k) {
+        const float2 cs = P.rope[size_t(pos) * half + pi];
+        out = even ? val * cs.x - other * cs.y : val * cs.x + other * cs.y;
       }
-      es.xch[j][m] = val[j];
-    }
-    wk_bar();
-    if (kind == PH_QKV) {
-      const int hd = P.hd, half = hd >> 1;
-      const int i = m % hd;
-      const int partner = i < half ? m + half : m - half;
-      const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int t = c0 + j;
-        if (t >= rows) continue;
-        const int pos = n0 + t;
-        float out = val[j];
-        if (is_q || is_k) {
-          const float other = es.xch[j][partner];
-          const float a = i < half ? val[j] : other, b = i < half ? other : val[j];
-          const float2 cs = P.rope[size_t(pos) * half + (i % half)];
-          out = i < half ? a * cs.x - b * cs.y : b * cs.x + a * cs.y;
-        }
-        const __nv_bfloat16 ob = __float2bfloat16_rn(out);
-        if (is_q) {
-          P.q[size_t(t) * P.qd + n] = ob;
-        } else {
-          const int cc = n - P.qd - (is_k ? 0 : P.kvd);
-          const int h = cc / hd;
-          const size_t page = size_t(P.page_table[pos / kPage]);
-          const size_t off = size_t(layer) * P.g.layer_stride() +
-                             ((page * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc % hd);
-          (is_k ? P.kpool : P.vpool)[off] = ob;
-        }
-      }
-    } else if (m < 64) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int t = c0 + j;
-        if (t >= rows) continue;
-        const float g = val[j], u = es.xch[j][m + 64];
-        P.act[size_t(t) * P.I + tile * 64 + m] = __float2bfloat16_rn(g / (1.0f + expf(-g)) * u);
+      const __nv_bfloat16 ob = __float2bfloat16_rn(out);
+      const int col = n - r + dim;  // original (unpermuted) output column
+      if (is_q) {
+        P.q[size_t(t) * P.qd + col] = ob;
+      } else {
+        const int cc = col - P.qd - (is_k ? 0 : P.kvd);
+        const int h = cc / hd;
+        const size_t page = size_t(P.page_table[pos / kPage]);
+        const size_t off = size_t(layer) * P.g.layer_stride() +
+                           ((page * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc % hd);
+        (is_k ? P.kpool : P.vpool)[off] = ob;
       }
     }
-    wk_bar();
+  } else if (kind == PH_GU) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = c0 + j;
+      const float val = t < rows ? v[j] * es.rstd[t] : 0.f;
+      const float up = __shfl_xor_sync(0xffffffffu, val, 1);
+      if (t < rows && (m & 1) == 0)
+        P.act[size_t(t) * P.I + tile * 64 + (m >> 1)] = __float2bfloat16_rn(val / (1.0f + expf(-val)) * up);
+    }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
 #pragma unroll
@@ -163,14 +190,9 @@ __device__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows,
         sq = xi * xi;
       }
       sq = warp_sum(sq);
-      if (lane == 0) es.red_v[q][j] = sq;
+      if (lane == 0 && t < rows) P.ssq_part[size_t(tile * 4 + q) * kMaxWindow + t] = sq;
     }
-    wk_bar();
-    if (m < 8 && c0 + m < rows)
-      P.ssq_part[size_t(tile) * kMaxWindow + c0 + m] =
-          ((es.red_v[0][m] + es.red_v[1][m]) + es.red_v[2][m]) + es.red_v[3][m];
-    wk_bar();
-  } else {  // PH_LM: logits = rstd * acc + bias; per-tile (max, lowest id)
+  } else {  // PH_LM: logits = rstd * acc + bias; per-quadrant (max, lowest id)
     const bool valid = n < P.vocab_local;
     const int vid = P.v_begin + n;
     const float b = valid ? P.lm_bias[vid] : 0.f;
@@ -184,54 +206,48 @@ __device__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows,
         li = vid;
       }
       warp_argmax(lv, li);
-      if (lane == 0) {
-        es.red_v[q][j] = lv;
-        es.red_i[q][j] = li;
-      }
+      if (lane == 0 && t < rows) argmax_merge(es.am_v[q][t], es.am_i[q][t], lv, li);
     }
-    wk_bar();
-    if (m < 8 && c0 + m < rows) {
-      float bv = es.red_v[0][m];
-      int bi = es.red_i[0][m];
-      for (int qq = 1; qq < 4; ++qq) argmax_merge(bv, bi, es.red_v[qq][m], es.red_i[qq][m]);
-      P.am_val[size_t(tile) * kMaxWindow + c0 + m] = bv;
-      P.am_idx[size_t(tile) * kMaxWindow + c0 + m] = bi;
-    }
-    wk_bar();
   }
 }
 
 // rstd of every row of the pass from the per-tile sums of squares of the
 // previous RESID phase (or the embed rstd), one warp per row, fixed tree.
-__device__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, EpiSmem& es) {
+__device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, EpiSmem& es) {
   const int ntiles = P.H / 128;
   for (int t = w; t < rows; t += 4) {
     if (from_embed) {
       if (lane == 0) es.rstd[t] = __ldcg(P.rstd0 + t);
     } else {
-      float a0 = lane < ntiles ? __ldcg(P.ssq_part + size_t(lane) * kMaxWindow + t) : 0.f;
-      float a1 = lane + 32 < ntiles ? __ldcg(P.ssq_part + size_t(lane + 32) * kMaxWindow + t) : 0.f;
-      const float ssq = warp_sum(a0 + a1);
+      // 4 quadrant partials per tile; lane sums entries lane, lane+32, ... in order
+      const int nparts = 4 * ntiles;
+      float a = 0.f;
+      for (int e = lane; e < nparts; e += 32) a += __ldcg(P.ssq_part + size_t(e) * kMaxWindow + t);
+      const float ssq = warp_sum(a);
       if (lane == 0) es.rstd[t] = 1.0f / sqrtf(ssq / float(P.H) + P.eps);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-__device__ void attention_unit(const MegaParams& P, int layer, int t, int kvh, int s, int n0, float* sm,
-                               int w, int lane, int* s_flag) {
-  const int pos = n0 + t;
-  const int nsplit = pos / kPage + 1;
+constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
+
+// One unit = (kv head, 64-token page s, block of up to kAttnRows query rows).
+// Per (row, q head): scores for the page's keys, page-local softmax stats and
+// P.V; the last page to finish for a (row, kv head) merges all pages in page
+// order. The per-(row, head) arithmetic does not depend on the block/pass.
+__device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, int t0, int t1, int kvh, int s, int n0, float* sm,
+                               int w, int lane, int* rflag) {
   const int hd = P.hd, grp = P.heads / P.kv_heads;
-  const int nkeys = min(kPage, pos + 1 - s * kPage);
-  float* Ks = sm;
-  float* Vs = Ks + kPage * (hd + 1);
-  float* Qs = Vs + kPage * hd;
+  const int kmax = min(kPage, n0 + t1 - 1 + 1 - s * kPage);  // keys needed by the last row of the block
+  float* Ks = sm;                     // [64][hd+1]
+  float* Vs = Ks + kPage * (hd + 1);  // [64][hd], 16-byte aligned rows
+  float* Qs = Vs + kPage * hd;        // [kAttnRows][grp][hd]
   const int tid = threadIdx.x - 64;
   const size_t page = size_t(P.page_table[s]);
   const size_t off = size_t(layer) * P.g.layer_stride() + (page * P.kv_heads + kvh) * kPage * hd;
   const int vpr = hd / 8;
-  for (int e = tid; e < nkeys * vpr; e += kWorkers) {
+  for (int e = tid; e < kmax * vpr; e += kWorkers) {
     const int j = e / vpr, d0 = (e % vpr) * 8;
     const uint4 kr = __ldcg(reinterpret_cast<const uint4*>(P.kpool + off + size_t(j) * hd + d0));
     const uint4 vr = __ldcg(reinterpret_cast<const uint4*>(P.vpool + off + size_t(j) * hd + d0));
@@ -243,71 +259,143 @@ __device__ void attention_unit(const MegaParams& P, int layer, int t, int kvh, i
       Vs[j * hd + d0 + i] = __bfloat162float(vb[i]);
     }
   }
-  const __nv_bfloat16* qrow = P.q + size_t(t) * P.qd + size_t(kvh) * grp * hd;
-  for (int e = tid; e < grp * hd; e += kWorkers) Qs[e] = __bfloat162float(__ldcg(qrow + e));
+  const int nrows = t1 - t0;
+  for (int e = tid; e < nrows * grp * hd; e += kWorkers) {
+    const int r = e / (grp * hd), rem = e % (grp * hd);
+    Qs[e] = __bfloat162float(__ldcg(P.q + size_t(t0 + r) * P.qd + size_t(kvh) * grp * hd + rem));
+  }
   wk_bar();
-  for (int hh = w; hh < grp; hh += 4) {
+  for (int pr = w; pr < nrows * grp; pr += 4) {
+    const int r = pr / grp, hh = pr % grp;
+    const int t = t0 + r, pos = n0 + t;
+    if (s > pos / kPage) continue;  // this page is beyond the row's causal range
+    const int nkeys = min(kPage, pos + 1 - s * kPage);
     const int h = kvh * grp + hh;
-    const float* qs = Qs + hh * hd;
+    const float* qs = Qs + (r * grp + hh) * hd;
     float sc[2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int j = lane + 32 * r;
-      float acc = 0.f;
+    for (int rr = 0; rr < 2; ++rr) {
+      const int j = lane + 32 * rr;
+      sc[rr] = -INFINITY;
       if (j < nkeys) {
         const float* kr = Ks + j * (hd + 1);
-        for (int d = 0; d < hd; ++d) acc = fmaf(qs[d], kr[d], acc);
-        sc[r] = acc * P.attn_scale;
-      } else {
-        sc[r] = -INFINITY;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 independent chains
+        for (int d = 0; d < hd; d += 4) {
+          a0 = fmaf(qs[d], kr[d], a0);
+          a1 = fmaf(qs[d + 1], kr[d + 1], a1);
+          a2 = fmaf(qs[d + 2], kr[d + 2], a2);
+          a3 = fmaf(qs[d + 3], kr[d + 3], a3);
+        }
+        sc[rr] = ((a0 + a1) + (a2 + a3)) * P.attn_scale;
       }
     }
-    const float m = warp_max(fmaxf(sc[0], sc[1]));
-    const float p0 = (lane < nkeys) ? expf(sc[0] - m) : 0.f;
-    const float p1 = (lane + 32 < nkeys) ? expf(sc[1] - m) : 0.f;
+    const float mx = warp_max(fmaxf(sc[0], sc[1]));
+    const float p0 = (lane < nkeys) ? expf(sc[0] - mx) : 0.f;
+    const float p1 = (lane + 32 < nkeys) ? expf(sc[1] - mx) : 0.f;
     const float l = warp_sum(p0 + p1);
     const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-    for (int d = lane; d < hd; d += 32) {
-      float acc = 0.f;
+    for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int j = 0; j < nkeys; ++j) {
         const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
-        acc = fmaf(pj, Vs[j * hd + d], acc);
+        const float4 vv = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
+        acc.x = fmaf(pj, vv.x, acc.x);
+        acc.y = fmaf(pj, vv.y, acc.y);
+        acc.z = fmaf(pj, vv.z, acc.z);
+        acc.w = fmaf(pj, vv.w, acc.w);
       }
-      P.o_part[slot * hd + d] = acc;
+      *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc;
     }
     if (lane == 0) {
-      P.ml_part[slot * 2] = m;
+      P.ml_part[slot * 2] = mx;
       P.ml_part[slot * 2 + 1] = l;
     }
   }
-  __threadfence();
   wk_bar();
-  if (tid == 0) {
-    unsigned* c = P.acnt + size_t(t) * P.kv_heads + kvh;
-    const unsigned old = atomicAdd(c, 1u);
-    *s_flag = old == unsigned(nsplit - 1);
-    if (*s_flag) *c = 0u;
+  // page arrival for every row of the block at once; the last page merges
+  if (tid < nrows) {
+    const int t = t0 + tid, pos = n0 + t;
+    rflag[tid] = 0;
+    if (s <= pos / kPage) {
+      unsigned* cnt = P.acnt + size_t(t) * P.kv_heads + kvh;
+      const unsigned old = atom_add_acq_rel(cnt, 1u);
+      if (old == unsigned(pos / kPage)) {
+        rflag[tid] = 1;
+        *cnt = 0u;
+      }
+    }
   }
   wk_bar();
-  if (*s_flag) {
-    __threadfence();
+  for (int r = 0; r < nrows; ++r) {
+    if (!rflag[r]) continue;
+    const int t = t0 + r, pos = n0 + t;
+    const int nsplit = pos / kPage + 1;
+    // merge: lane sp owns page sp for the scalars (fixed butterfly); the
+    // output sums run over pages in order
     for (int hh = w; hh < grp; hh += 4) {
       const int h = kvh * grp + hh;
       const size_t base = (size_t(t) * P.heads + h) * P.max_splits_attn;
       float M = -INFINITY;
-      for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
-      for (int d = lane; d < hd; d += 32) {
-        float L = 0.f, acc = 0.f;
+      for (int sp = lane; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
+      M = warp_max(M);
+      float Lp = 0.f;
+      for (int sp = lane; sp < nsplit; sp += 32)
+        Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
+      const float L = warp_sum(Lp);
+      for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int sp = 0; sp < nsplit; ++sp) {
           const float f = expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
-          L = fmaf(__ldcg(P.ml_part + (base + sp) * 2 + 1), f, L);
-          acc = fmaf(__ldcg(P.o_part + (base + sp) * hd + d), f, acc);
+          const float4 o = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp) * hd + d4));
+          acc.x = fmaf(o.x, f, acc.x);
+          acc.y = fmaf(o.y, f, acc.y);
+          acc.z = fmaf(o.z, f, acc.z);
+          acc.w = fmaf(o.w, f, acc.w);
         }
-        P.attn[size_t(t) * P.qd + size_t(h) * hd + d] = __float2bfloat16_rn(acc / L);
+        __nv_bfloat16* dst = P.attn + size_t(t) * P.qd + size_t(h) * hd + d4;
+        dst[0] = __float2bfloat16_rn(acc.x / L);
+        dst[1] = __float2bfloat16_rn(acc.y / L);
+        dst[2] = __float2bfloat16_rn(acc.z / L);
+        dst[3] = __float2bfloat16_rn(acc.w / L);
       }
     }
   }
   wk_bar();
+}
+
+// Sum a split tile's piece partials (in CTA order, all loads in flight) for
+// rows [r_lo, r_hi) and run the phase's finishing math on them.
+// Partial slot of CTA cc's piece of `tile` (slot 0 = the CTA's first tile).
+__device__ __forceinline__ int piece_off(int cc, int tile, const Gemm& g, int m) {
+  return (cc * 2 + (sk_start(cc, g.G, g.T) / g.KB == tile ? 0 : 1)) * kMaxWindow * 128 + m;
+}
+
+// Sum a split tile's piece partials (pieces = CTAs c_first.., in CTA order,
+// all loads in flight) for rows [r_lo, r_hi) and run the finishing math.
+__device__ __forceinline__ void finish_from_pieces(const MegaParams& P, int kind, int layer, int r_lo, int r_hi, int n0,
+                                                   int tile, int m, int q, int lane, int c_first, int npieces,
+                                                   const Gemm& g, EpiSmem& es) {
+  int off[8];
+#pragma unroll
+  for (int pc = 0; pc < 8; ++pc) off[pc] = pc < npieces ? piece_off(c_first + pc, tile, g, m) : 0;
+  for (int c0 = r_lo; c0 < r_hi; c0 += 8) {
+    float tmp[8][8];
+#pragma unroll
+    for (int pc = 0; pc < 8; ++pc)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        tmp[pc][j] = (pc < npieces && c0 + j < r_hi) ? __ldcg(P.part + off[pc] + size_t(c0 + j) * 128) : 0.f;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float acc = tmp[0][j];
+#pragma unroll
+      for (int pc = 1; pc < 8; ++pc)
+        if (pc < npieces) acc += tmp[pc][j];
+      v[j] = acc;
+    }
+    finish_chunk(P, kind, layer, r_hi, n0, tile, m, q, lane, c0, v, es);
+  }
 }
 
 }  // namespace
@@ -352,7 +440,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   const uint32_t tmem = tmem_holder;
   const int n0 = P.ctx->n0;
   const int rows = P.ctx->rows;
-  const int nphases = 2 + 5 * P.L;
+  const int nphases = 3 + 5 * P.L;
 
   if (warp == 0) {
     // ======================= TMA producer =======================
@@ -363,9 +451,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         uint32_t it = 0;
         for (int p = 1; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
-          if (kind == PH_ATTN) continue;
+          if (kind == PH_ATTN || kind == PH_FINAL) continue;
           const Gemm g = gemm_of(P, kind);
-          const int kb_lo = sk_start(c, G, g.T), kb_hi = sk_start(c + 1, G, g.T);
+          const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
           const int nk = kb_hi - kb_lo;
           const CUtensorMap* wm = wmap_of(P, p, kind);
           const CUtensorMap* xm = xmap_of(P, kind);
@@ -380,6 +468,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             tma_load_2d(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128);
           }
           grid_wait(P.bar, unsigned(G) * unsigned(p));  // activations of this phase are complete
+          stamp(P, p, c, G, 0);
           fence_proxy_async_global();
           for (int i = 0; i < pre; ++i) {
             const uint32_t s = (it + i) % ST;
@@ -407,9 +496,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         uint32_t it = 0, acc_it = 0;
         for (int p = 1; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
-          if (kind == PH_ATTN) continue;
+          if (kind == PH_ATTN || kind == PH_FINAL) continue;
           const Gemm g = gemm_of(P, kind);
-          const int kb_lo = sk_start(c, G, g.T), kb_hi = sk_start(c + 1, G, g.T);
+          const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
           int x = kb_lo;
           while (x < kb_hi) {  // one piece per tile touched by this CTA
             const int tile = x / g.KB;
@@ -433,6 +522,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             ++acc_it;
             x = piece_hi;
           }
+          stamp(P, p, c, G, 3);
         }
       }
     }
@@ -480,23 +570,52 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       if (tid == 0) P.rstd0[t] = 1.0f / sqrtf((((es.red_v[0][0] + es.red_v[1][0]) + es.red_v[2][0]) + es.red_v[3][0]) / float(P.H) + P.eps);
       wk_bar();
     }
-    __threadfence();
     wk_bar();
-    if (tid == 0) grid_arrive(P.bar);
+    if (tid == 0) {
+      stamp(P, 0, c, G, 2);
+      grid_arrive(P.bar);
+    }
     for (int p = 1; p < nphases; ++p) {
       const int kind = phase_kind(p, P.L);
       const int layer = kind == PH_LM ? P.L - 1 : (p - 1) / 5;
-      if (tid == 0) grid_wait(P.bar, unsigned(G) * unsigned(p));
+      if (tid == 0) {
+        grid_wait(P.bar, unsigned(G) * unsigned(p));
+        stamp(P, p, c, G, 1);
+      }
       wk_bar();
       if (P.ctx->stop) break;
-      if (kind == PH_ATTN) {
+      if (kind == PH_FINAL) {
+        // argmax of every row over the per-CTA partials of the LM phase;
+        // rows are spread over CTAs (t = c, c+G, ...), one warp per row
+        for (int t = c * 4 + w; t < rows; t += 4 * G) {
+          float bv = -INFINITY;
+          int bi = 0x7fffffff;
+          for (int cc = lane; cc < G; cc += 32)
+            argmax_merge(bv, bi, __ldcg(P.am_val + size_t(cc) * kMaxWindow + t), __ldcg(P.am_idx + size_t(cc) * kMaxWindow + t));
+          warp_argmax(bv, bi);
+          if (lane == 0) {
+            P.argmax_pos[n0 + t] = bi;
+            if (P.keys) {
+              unsigned uu = __float_as_uint(bv);
+              uu = (uu & 0x80000000u) ? ~uu : (uu | 0x80000000u);
+              P.keys[t] = (static_cast<unsigned long long>(uu) << 32) | (0xFFFFFFFFull - unsigned(bi));
+            }
+            if (t == 0 && P.advance) {  // decode: one row, handled by CTA 0 warp 0
+              P.ctx->n0 = n0 + 1;
+              P.ctx->step += 1;
+            }
+          }
+        }
+      } else if (kind == PH_ATTN) {
         const int npages = (n0 + rows - 1) / kPage + 1;
-        const int units = rows * P.kv_heads * npages;
+        const int nblocks = (rows + kAttnRows - 1) / kAttnRows;
+        const int units = nblocks * P.kv_heads * npages;
         for (int u = c; u < units; u += G) {
           const int s = u % npages, r = u / npages;
-          const int kvh = r % P.kv_heads, t = r / P.kv_heads;
-          if (s > (n0 + t) / kPage) continue;
-          attention_unit(P, layer, t, kvh, s, n0, attn_sm, w, lane, &es.flag);
+          const int kvh = r % P.kv_heads, blk = r / P.kv_heads;
+          const int t0 = blk * kAttnRows, t1 = min(rows, t0 + kAttnRows);
+          if (s > (n0 + t1 - 1) / kPage) continue;  // no row of the block reaches this page
+          attention_unit(P, layer, t0, t1, kvh, s, n0, attn_sm, w, lane, es.rflag);
         }
       } else {
         if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {
@@ -506,19 +625,38 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             for (int t = tid; t < rows; t += kWorkers) P.rstd_cache[n0 + t] = es.rstd[t];
         }
         const Gemm g = gemm_of(P, kind);
-        const int kb_lo = sk_start(c, G, g.T), kb_hi = sk_start(c + 1, G, g.T);
+        const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
         const int first_tile = kb_lo / g.KB;
+        // per-phase arrival counters (zeroed before the pass): no resets, no reuse races
+        unsigned* cnt = P.tile_cnt + size_t(p) * P.max_tiles;
+        // Few rows (decode): the last piece to arrive finalizes the whole tile.
+        // Many rows (verify/prefill): every piece publishes without blocking,
+        // then each piece's CTA finalizes its own share of the rows.
+        const bool spread = rows > 8;
+        int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
+        if (kind == PH_LM) {
+          for (int e = tid; e < 4 * kMaxWindow; e += kWorkers) {
+            es.am_v[e / kMaxWindow][e % kMaxWindow] = -INFINITY;
+            es.am_i[e / kMaxWindow][e % kMaxWindow] = 0x7fffffff;
+          }
+          wk_bar();
+        }
         int x = kb_lo;
         while (x < kb_hi) {
           const int tile = x / g.KB;
           const int piece_hi = min(kb_hi, (tile + 1) * g.KB);
-          const int c_first = sk_owner(tile * g.KB, G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, G, g.T);
-          // CTAs between c_first and c_last with an empty range (T < G) hold no piece
-          int npieces = 0;
-          for (int cc = c_first; cc <= c_last; ++cc) npieces += sk_start(cc, G, g.T) < sk_start(cc + 1, G, g.T);
+          const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
+          const int npieces = c_last - c_first + 1;  // <= 8 by the choice of g.G
+          {
+            const int n = tile * 128 + m;
+            if (kind == PH_O || kind == PH_D) prefetch_l1(P.x + n);
+            if (kind == PH_QKV) prefetch_l1(P.rope + size_t(n0) * (P.hd >> 1) + ((n % P.hd) >> 1));
+            if (kind == PH_LM && n < P.vocab_local) prefetch_l1(P.lm_bias + P.v_begin + n);
+          }
           const uint32_t b = acc_it & 1, aph = (acc_it >> 1) & 1;
           mbar_wait(acc_full0 + 8 * b, aph);
           tc_fence_after();
+          if (tid == 0) stamp(P, p, c, G, 4);
           const uint32_t trow = tmem + b * uint32_t(P.acc_cols) + (uint32_t(q * 32) << 16);
           if (npieces == 1) {
             for (int c0 = 0; c0 < rows; c0 += 8) {
@@ -530,8 +668,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             wk_bar();
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
           } else {
-            const int slot = tile == first_tile ? 0 : 1;
-            float* mine = P.part + (size_t(c * 2 + slot) * kMaxWindow) * 128 + m;
+            float* mine = P.part + piece_off(c, tile, g, m);
             for (int c0 = 0; c0 < rows; c0 += 8) {
               float v[8];
               tmem_ld8(trow + c0, v);
@@ -540,89 +677,55 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
                 if (c0 + j < rows) mine[size_t(c0 + j) * 128] = v[j];
             }
             tc_fence_before();
-            __threadfence();
             wk_bar();
             if (tid == 0) {
               mbar_arrive(acc_empty0 + 8 * b);
-              const unsigned old = atomicAdd(P.tile_cnt + tile, 1u);
+              const unsigned old = atom_add_acq_rel(cnt + tile, 1u);
               es.flag = old == unsigned(npieces - 1);
-              if (es.flag) P.tile_cnt[tile] = 0u;
             }
             wk_bar();
-            if (es.flag) {
-              __threadfence();
-              for (int c0 = 0; c0 < rows; c0 += 8) {
-                float v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = 0.f;
-                bool first_piece = true;
-                for (int cc = c_first; cc <= c_last; ++cc) {
-                  if (sk_start(cc, G, g.T) == sk_start(cc + 1, G, g.T)) continue;
-                  const int sl = (sk_start(cc, G, g.T) / g.KB == tile) ? 0 : 1;
-                  const float* src = P.part + (size_t(cc * 2 + sl) * kMaxWindow) * 128 + m;
-                  float tmp[8];
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) tmp[j] = (c0 + j < rows) ? __ldcg(src + size_t(c0 + j) * 128) : 0.f;
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) v[j] = first_piece ? tmp[j] : v[j] + tmp[j];
-                  first_piece = false;
-                }
-                finish_chunk(P, kind, layer, rows, n0, tile, m, q, lane, c0, v, es);
-              }
+            if (spread) {
+              if (dtile0 < 0) dtile0 = tile; else dtile1 = tile;
+            } else if (es.flag) {
+              finish_from_pieces(P, kind, layer, 0, rows, n0, tile, m, q, lane, c_first, npieces, g, es);
             }
           }
           ++acc_it;
           x = piece_hi;
         }
-        if (kind == PH_LM) {
-          // grid-wide argmax over vocab tiles: the last CTA to finish reduces
-          __threadfence();
-          wk_bar();
+        if (tid == 0) stamp(P, p, c, G, 5);
+        // second pass (many rows): wait for each split tile's pieces, finalize this CTA's row share
+        for (int d = 0; d < 2; ++d) {
+          const int tile = d == 0 ? dtile0 : dtile1;
+          if (tile < 0) continue;
+          const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
+          const int npieces = c_last - c_first + 1, my_idx = c - c_first;
+          const int r_lo = my_idx * rows / npieces, r_hi = (my_idx + 1) * rows / npieces;
           if (tid == 0) {
-            const unsigned old = atomicAdd(P.lm_cnt, 1u);
-            es.flag = old == unsigned(G - 1);
-            if (es.flag) *P.lm_cnt = 0u;
+            grid_wait(cnt + tile, unsigned(npieces));
+            if (d == 0) stamp(P, p, c, G, 7);
           }
           wk_bar();
-          if (es.flag) {
-            __threadfence();
-            const int ntiles = g.tiles;
-            for (int t = w; t < rows; t += 4) {
-              float bv = -INFINITY;
-              int bi = 0x7fffffff;
-              for (int t0 = 0; t0 < ntiles; t0 += 32 * 8) {
-                float vv[8];
-                int ii[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  const int tt = t0 + u * 32 + lane;
-                  vv[u] = tt < ntiles ? __ldcg(P.am_val + size_t(tt) * kMaxWindow + t) : -INFINITY;
-                  ii[u] = tt < ntiles ? __ldcg(P.am_idx + size_t(tt) * kMaxWindow + t) : 0x7fffffff;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) argmax_merge(bv, bi, vv[u], ii[u]);
-              }
-              warp_argmax(bv, bi);
-              if (lane == 0) {
-                P.argmax_pos[n0 + t] = bi;
-                if (P.keys) {
-                  unsigned uu = __float_as_uint(bv);
-                  uu = (uu & 0x80000000u) ? ~uu : (uu | 0x80000000u);
-                  P.keys[t] = (static_cast<unsigned long long>(uu) << 32) | (0xFFFFFFFFull - unsigned(bi));
-                }
-              }
-            }
-            wk_bar();
-            if (tid == 0 && P.advance) {
-              P.ctx->n0 = n0 + 1;
-              P.ctx->step += 1;
-            }
+          if (r_lo < r_hi) finish_from_pieces(P, kind, layer, r_lo, r_hi, n0, tile, m, q, lane, c_first, npieces, g, es);
+        }
+        if (tid == 0) stamp(P, p, c, G, 6);
+        if (kind == PH_LM) {
+          // this CTA's (max, lowest id) per row: its 4 warp slots merged in order
+          wk_bar();
+          for (int t = tid; t < rows; t += kWorkers) {
+            float bv = es.am_v[0][t];
+            int bi = es.am_i[0][t];
+            for (int qq = 1; qq < 4; ++qq) argmax_merge(bv, bi, es.am_v[qq][t], es.am_i[qq][t]);
+            P.am_val[size_t(c) * kMaxWindow + t] = bv;
+            P.am_idx[size_t(c) * kMaxWindow + t] = bi;
           }
         }
       }
-      __threadfence();
       wk_bar();
-      if (tid == 0) grid_arrive(P.bar);
+      if (tid == 0) {
+        stamp(P, p, c, G, 2);
+        grid_arrive(P.bar);
+      }
     }
   }
   tc_fence_before();
@@ -634,8 +737,15 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
 }
 
 int mega_stages(int ntok, int attn_floats) {
+  static int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa{};
+    static_smem = cudaFuncGetAttributes(&fa, mega_kernel) == cudaSuccess ? int(fa.sharedSizeBytes) : 16 * 1024;
+  }
   const int stage = kTileABytes + ntok * 128;
-  const int avail = 222 * 1024 - attn_floats * 4 - 2048;
+  // 227 KB per CTA minus static shared memory, attention staging and the
+  // 1 KB alignment slack
+  const int avail = 227 * 1024 - static_smem - attn_floats * 4 - 1024;
   int s = avail / stage;
   return s > 8 ? 8 : s;
 }
@@ -645,10 +755,11 @@ int mega_smem_bytes(int ntok, int stages, int attn_floats) {
 }
 
 cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  static int attr_smem = -1;
+  if (attr_smem != smem) {
+    const cudaError_t e = cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_smem = smem;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -661,6 +772,13 @@ cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st
   cfg.attrs = attr1;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, mega_kernel, P);
+}
+
+int mega_max_blocks_per_sm(int smem) {
+  if (cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel, 192, smem) != cudaSuccess) return 0;
+  return n;
 }
 
 }  // namespace ps

@@ -105,7 +105,7 @@ struct WEntry {
   void* ptr;
   int64_t count;
   int64_t cols = 0;
-  int interleave_off = -1;  // >= 0: rows stored interleaved in 64-row blocks (gate/up)
+  RowPerm perm{};           // storage row of source row r = perm.dst(r) (bf16 fused matrices)
 };
 
 constexpr int kCtxSlots = 64;
@@ -207,7 +207,10 @@ struct ps_handle {
   std::vector<int> xmaps_ready;             // per ntok/16
   __nv_bfloat16* qkv_bias_all = nullptr;
   float* mega_part = nullptr;
-  unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [64..] tile counters
+  unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [64..] per-phase tile counters
+  int mega_max_tiles = 0;
+  size_t mega_cnt_words = 0;
+  unsigned long long* mega_trace = nullptr;  // PS_TRACE=1: per-phase globaltimer stamps
   // vocab sharding (c4)
   unsigned long long* keys = nullptr;      // [kMaxWindow] packed (value, id) of this pass
   unsigned long long* keys_pos = nullptr;  // [seq_rows] per position
@@ -235,7 +238,9 @@ struct ps_handle {
   T* dalloc(size_t n) {
     void* p = nullptr;
     if (cudaMalloc(&p, n * sizeof(T) + 256) != cudaSuccess) return nullptr;
-    cudaMemset(p, 0, n * sizeof(T) + 256);
+    // stream-ordered with the init kernels (a legacy-stream memset would race
+    // them: the runtime stream is non-blocking)
+    cudaMemsetAsync(p, 0, n * sizeof(T) + 256, st);
     allocs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -381,7 +386,7 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
 
 int launches_per_pass(const ps_handle* h) {
   if (h->mega) return 1 + (h->cfg.vocab_shards > 1 ? 1 : 0);
-  return h->bf16 ? 1 + 5 * h->L + 1 : 1 + 10 * h->L + 2;
+  return 1 + 10 * h->L + 2;
 }
 
 
@@ -400,7 +405,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   using bf = __nv_bfloat16;
   const int ntok = round_up(std::max(max_rows, 1), 16);
   const int grp = h->nh / h->nkv;
-  const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + grp * h->hd;
+  const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + 4 * grp * h->hd;
   MegaParams P{};
   P.ctx = ctx;
   P.decode = decode ? 1 : 0;
@@ -443,107 +448,24 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.acnt = h->acnt;
   P.part = h->mega_part;
   P.tile_cnt = h->mega_cnt + 64;
+  P.max_tiles = h->mega_max_tiles;
   P.lm_cnt = h->mega_cnt + 1;
   P.am_val = h->am_val;
   P.am_idx = h->am_idx;
   P.keys = sharded ? h->keys : nullptr;
   P.bar = h->mega_cnt;
-  cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned), h->st);
+  P.trace = h->mega_trace;
+  cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned) * h->mega_cnt_words, h->st);
   prof_mark(h, 7);
-  launch_mega(P, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
+  const cudaError_t e = launch_mega(P, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
+  if (e != cudaSuccess) std::fprintf(stderr, "predgen_b200: megakernel launch failed: %s\n", cudaGetErrorString(e));
   if (sharded) enqueue_shard_merge(h, ctx, max_rows, decode);
   prof_mark(h, 6);
 }
 
-// bf16 decode chain: 5 launches per layer, all PDL-chained (weights of the
-// next GEMM stream while the previous kernel drains).
 void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode) {
-  using bf = __nv_bfloat16;
-  if (h->mega) return enqueue_mega(h, ctx, max_rows, tok_in, decode);
-  cudaStream_t st = h->st;
-  const int ntok = round_up(std::max(max_rows, 1), 16);
-  const ActDescs* ad = act_descs(h, ntok);
-  bf* xb = static_cast<bf*>(h->xn);
-  unsigned* cnt_qkv = h->counters;
-  unsigned* cnt_o = h->counters + 1024;
-  unsigned* cnt_gu = h->counters + 2048;
-  unsigned* cnt_d = h->counters + 3072;
-  unsigned* gcnt = h->counters + 4096;  // [0] o, [1] down, [2] lm head
-  const bool pdl = true;
-  prof_mark(h, 0);
-  launch_embed_bf16(ctx, max_rows, tok_in, h->tokens_dev, h->argmax_pos, static_cast<const bf*>(h->embed), h->x, xb,
-                    h->rstd, h->H, h->cfg.rms_eps, st, pdl);
-  for (int l = 0; l < h->L; ++l) {
-    const Layer& ly = h->layers[l];
-    TcEpilogue e;
-    e.mode = TC_EPI_QKV;
-    e.part = h->part;
-    e.tile_cnt = cnt_qkv;
-    e.rstd_in = h->rstd;
-    e.bias = static_cast<const bf*>(ly.bqkv);
-    e.rope = h->rope;
-    e.q = static_cast<bf*>(h->q);
-    e.kpool = static_cast<bf*>(h->kpool);
-    e.vpool = static_cast<bf*>(h->vpool);
-    e.page_table = h->d_page_table;
-    e.g = h->g;
-    e.layer = l;
-    e.q_dim = h->qd;
-    e.kv_dim = h->kvd;
-    prof_mark(h, 1);
-    launch_tc(ctx, &ly.qkv.tm, &ad->xn, ly.qkv.N, ly.qkv.K, ly.qkv.splits, ntok, 0, e, st, pdl);
-    prof_mark(h, 2);
-    launch_attention_bf16(ctx, max_rows, max_pos, static_cast<const bf*>(h->q), static_cast<const bf*>(h->kpool),
-                          static_cast<const bf*>(h->vpool), h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part,
-                          h->acnt, static_cast<bf*>(h->attn), st, pdl);
-    TcEpilogue r;
-    r.mode = TC_EPI_RESID;
-    r.part = h->part;
-    r.tile_cnt = cnt_o;
-    r.grid_cnt = gcnt + 0;
-    r.x = h->x;
-    r.xb_out = xb;
-    r.ssq_part = h->ssq_part;
-    r.rstd_out = h->rstd;
-    r.hidden = h->H;
-    r.eps = h->cfg.rms_eps;
-    prof_mark(h, 3);
-    launch_tc(ctx, &ly.o.tm, &ad->attn, ly.o.N, ly.o.K, ly.o.splits, ntok, 0, r, st, pdl);
-    TcEpilogue g;
-    g.mode = TC_EPI_SWIGLU;
-    g.part = h->part;
-    g.tile_cnt = cnt_gu;
-    g.rstd_in = h->rstd;
-    g.act = static_cast<bf*>(h->act);
-    g.inter = h->I;
-    prof_mark(h, 4);
-    launch_tc(ctx, &ly.gu.tm, &ad->xn, ly.gu.N, ly.gu.K, ly.gu.splits, ntok, 0, g, st, pdl);
-    const bool last = l == h->L - 1;
-    r.tile_cnt = cnt_d;
-    r.grid_cnt = gcnt + 1;
-    r.xb_out = last ? static_cast<bf*>(h->hn_cache) : xb;
-    r.xb_out_pos = last ? 1 : 0;
-    r.rstd_out = last ? h->rstd_cache : h->rstd;
-    r.rstd_out_pos = last ? 1 : 0;
-    prof_mark(h, 5);
-    launch_tc(ctx, &ly.d.tm, &ad->act, ly.d.N, ly.d.K, ly.d.splits, ntok, 0, r, st, pdl);
-  }
-  TcEpilogue a;
-  a.mode = TC_EPI_ARGMAX;
-  a.grid_cnt = gcnt + 2;
-  a.rstd_in = h->rstd_cache;
-  a.lbias = h->lm_bias;
-  a.v_begin = h->v_begin;
-  a.am_val = h->am_val;
-  a.am_idx = h->am_idx;
-  a.argmax_pos = h->argmax_pos;
-  const bool sharded = h->cfg.vocab_shards > 1;
-  a.packed_out = sharded ? h->keys : nullptr;
-  a.advance = (decode && !sharded) ? 1 : 0;
-  prof_mark(h, 6);
-  launch_tc(ctx, &h->tm_head, &ad->hn, h->v_count, h->H, 1, ntok, 1, a, st, pdl);
-  if (sharded) enqueue_shard_merge(h, ctx, max_rows, decode);
-  prof_mark(h, 7);
+  (void)max_pos;
+  enqueue_mega(h, ctx, max_rows, tok_in, decode);
 }
 
 // decode == true: 1-row step whose token is the previous row's argmax; the
@@ -772,18 +694,31 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     };
     if (!setup(ly.qkv, qd + 2 * kvd, H) || !setup(ly.o, H, qd) || !setup(ly.gu, 2 * I, H) || !setup(ly.d, H, I))
       return bad("layer weights");
-    init_tensor(h, ly.qkv.w, size_t(qd) * H, 0, layer_tid(l, WQ));
-    init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd) * H), size_t(kvd) * H, 0, layer_tid(l, WK));
-    init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd + kvd) * H), size_t(kvd) * H, 0, layer_tid(l, WV));
+    if (h->bf16) {
+      // q/k/v rows stored with RoPE pairs adjacent (kHeadPairs), see kernels.h
+      auto* w = static_cast<__nv_bfloat16*>(ly.qkv.w);
+      const int bases[3] = {0, qd, qd + kvd}, nrows[3] = {qd, kvd, kvd}, ids[3] = {WQ, WK, WV};
+      for (int k = 0; k < 3; ++k) {
+        RowPerm pm{RowPerm::kHeadPairs, h->hd, 0, bases[k]};
+        launch_init_rows_permuted(w, nrows[k], H, pm, c.seed, layer_tid(l, ids[k]), 0.02, h->st);
+        WEntry we{layer_tid(l, ids[k]), w, int64_t(nrows[k]) * H, H, pm};
+        h->wreg.push_back(we);
+      }
+    } else {
+      init_tensor(h, ly.qkv.w, size_t(qd) * H, 0, layer_tid(l, WQ));
+      init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd) * H), size_t(kvd) * H, 0, layer_tid(l, WK));
+      init_tensor(h, offset_ptr(h, ly.qkv.w, size_t(qd + kvd) * H), size_t(kvd) * H, 0, layer_tid(l, WV));
+    }
     init_tensor(h, ly.o.w, size_t(H) * qd, 0, layer_tid(l, WO));
     if (h->bf16) {
       // gate/up rows interleaved in 64-row blocks so one 128-row GEMM tile
       // holds matching gate and up features (SwiGLU in the GEMM epilogue)
       auto* gu = static_cast<__nv_bfloat16*>(ly.gu.w);
-      launch_init_rows_interleaved(gu, I, H, 64, 0, c.seed, layer_tid(l, WGATE), 0.02, h->st);
-      launch_init_rows_interleaved(gu, I, H, 64, 64, c.seed, layer_tid(l, WUP), 0.02, h->st);
-      h->wreg.push_back({layer_tid(l, WGATE), gu, int64_t(I) * H, H, 0});
-      h->wreg.push_back({layer_tid(l, WUP), gu, int64_t(I) * H, H, 64});
+      const RowPerm pg{RowPerm::kGateUp, 0, 0, 0}, pu{RowPerm::kGateUp, 0, 1, 0};
+      launch_init_rows_permuted(gu, I, H, pg, c.seed, layer_tid(l, WGATE), 0.02, h->st);
+      launch_init_rows_permuted(gu, I, H, pu, c.seed, layer_tid(l, WUP), 0.02, h->st);
+      h->wreg.push_back({layer_tid(l, WGATE), gu, int64_t(I) * H, H, pg});
+      h->wreg.push_back({layer_tid(l, WUP), gu, int64_t(I) * H, H, pu});
     } else {
       init_tensor(h, ly.gu.w, size_t(I) * H, 0, layer_tid(l, WGATE));
       init_tensor(h, offset_ptr(h, ly.gu.w, size_t(I) * H), size_t(I) * H, 0, layer_tid(l, WUP));
@@ -793,9 +728,20 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       ly.bqkv = h->qkv_bias_all ? static_cast<void*>(h->qkv_bias_all + size_t(l) * (qd + 2 * kvd))
                                 : alloc_weights(h, size_t(qd + 2 * kvd));
       if (!ly.bqkv) return bad("bias");
-      init_tensor(h, ly.bqkv, qd, 0, layer_tid(l, BQ));
-      init_tensor(h, offset_ptr(h, ly.bqkv, qd), kvd, 0, layer_tid(l, BK));
-      init_tensor(h, offset_ptr(h, ly.bqkv, qd + kvd), kvd, 0, layer_tid(l, BV));
+      if (h->bf16) {
+        auto* b = static_cast<__nv_bfloat16*>(ly.bqkv);
+        const int bases[3] = {0, qd, qd + kvd}, nrows[3] = {qd, kvd, kvd}, ids[3] = {BQ, BK, BV};
+        for (int k = 0; k < 3; ++k) {
+          RowPerm pm{RowPerm::kHeadPairs, h->hd, 0, bases[k]};
+          launch_init_rows_permuted(b, nrows[k], 1, pm, c.seed, layer_tid(l, ids[k]), 0.02, h->st);
+          WEntry we{layer_tid(l, ids[k]), b, int64_t(nrows[k]), 1, pm};
+          h->wreg.push_back(we);
+        }
+      } else {
+        init_tensor(h, ly.bqkv, qd, 0, layer_tid(l, BQ));
+        init_tensor(h, offset_ptr(h, ly.bqkv, qd), kvd, 0, layer_tid(l, BK));
+        init_tensor(h, offset_ptr(h, ly.bqkv, qd + kvd), kvd, 0, layer_tid(l, BV));
+      }
     }
     if (h->bf16) {
       bool ok = encode_tma_2d_bf16(&ly.qkv.tm, ly.qkv.w, H, ly.qkv.N, 64, kTileTc);
@@ -836,8 +782,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->ml_part = h->dalloc<float>(size_t(kMaxWindow) * h->nh * max_splits_attn * 2);
   h->hn_cache = alloc_weights(h, seq_rows * H);
   h->am_tiles = h->bf16 ? (h->v_count + kTileTc - 1) / kTileTc : (h->v_count + kLmTileF32 - 1) / kLmTileF32;
-  h->am_val = h->dalloc<float>(size_t(h->am_tiles) * kMaxWindow);
-  h->am_idx = h->dalloc<int>(size_t(h->am_tiles) * kMaxWindow);
+  // bf16: one partial per 32-row warp quadrant of each 128-row vocab tile
+  // bf16: one partial per CTA of the megakernel (<= 4 per vocab tile covers both uses)
+  h->am_val = h->dalloc<float>(size_t(std::max(h->am_tiles * (h->bf16 ? 4 : 1), 1024)) * kMaxWindow);
+  h->am_idx = h->dalloc<int>(size_t(std::max(h->am_tiles * (h->bf16 ? 4 : 1), 1024)) * kMaxWindow);
   h->argmax_pos = h->dalloc<int>(seq_rows);
   h->tokens_dev = h->dalloc<int>(seq_rows);
   h->term_mask = h->dalloc<unsigned char>(V);
@@ -847,7 +795,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->d_res = h->dalloc<int>(4);
   h->rstd = h->dalloc<float>(kMaxWindow);
   h->rstd_cache = h->dalloc<float>(seq_rows);
-  h->ssq_part = h->dalloc<float>(size_t(H / kTileTc + 1) * kMaxWindow);
+  h->ssq_part = h->dalloc<float>(size_t(4) * (H / kTileTc + 1) * kMaxWindow);
   h->counters = h->dalloc<unsigned>(4096 + 64);
   h->acnt = h->dalloc<unsigned>(size_t(kMaxWindow) * h->nkv);
   if (!h->rstd || !h->rstd_cache || !h->ssq_part || !h->counters || !h->acnt) return bad("bf16 chain buffers");
@@ -866,16 +814,20 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       !h->d_cand || !h->d_res || !h->d_ctx || !h->d_ctx_aux || !h->h_ctx || !h->h_tok || !h->h_res ||
       !h->h_argmax || !h->h_steps_tok)
     return bad("workspace");
-  h->mega = h->bf16 && c.reserved[0] == 0;
+  h->mega = h->bf16;
   if (h->mega) {
     int dev_sms = 0;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
     h->sms = dev_sms > 0 ? dev_sms : 148;
     h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128);
-    h->mega_cnt = h->dalloc<unsigned>(64 + 2048);
+    h->mega_max_tiles = (std::max(std::max(h->qd + 2 * h->kvd, 2 * h->I), std::max(h->H, h->v_count)) + 127) / 128;
+    h->mega_cnt_words = 64 + size_t(3 + 5 * h->L) * h->mega_max_tiles;
+    h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
     h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
     if (!h->mega_part || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
+    if (const char* tr = std::getenv("PS_TRACE"); tr && tr[0] == '1')
+      h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 12);
     std::vector<CUtensorMap> wm(size_t(4) * h->L + 1);
     for (int l = 0; l < h->L; ++l) {
       std::memcpy(&wm[4 * l + 0], h->layers[l].qkv.tm.bytes, sizeof(CUtensorMap));
@@ -895,6 +847,14 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       std::memcpy(&xm[4 * k + 3], ad->hn.bytes, sizeof(CUtensorMap));
     }
     cudaMemcpy(h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
+    // every pass width must fit one CTA per SM (co-residency of the grid)
+    const int grp = h->nh / h->nkv;
+    const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + 4 * grp * h->hd;
+    for (int ntok = 16; ntok <= kMaxWindow; ntok += 16) {
+      const int st = mega_stages(ntok, attn_floats);
+      if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats)) < 1)
+        return (ps_destroy(h), fail(PS_ERR_CUDA, "megakernel does not fit one CTA per SM"));
+    }
   }
   {
     // RoPE table (rotate-half pairs): angle = pos * theta^(-2i/hd), in fp64.
@@ -911,7 +871,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     tm[1] = tm[2] = tm[3] = 1;
     cudaMemcpy(h->term_mask, tm.data(), V, cudaMemcpyHostToDevice);
   }
-  if (cudaStreamSynchronize(h->st) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return (ps_destroy(h), fail(PS_ERR_CUDA, "device initialisation failed"));
   *out = h;
   return PS_OK;
@@ -1125,11 +1085,11 @@ int ps_read_weights(ps_handle* h, int32_t tid, int64_t offset, int64_t count, fl
   for (const WEntry& e : h->wreg) {
     if (e.tid != tid) continue;
     if (offset + count > e.count) return fail(PS_ERR_INVALID, "range outside tensor");
-    if (e.interleave_off >= 0) {
+    if (e.perm.kind != RowPerm::kIdentity) {
       std::vector<uint16_t> row(e.cols);
       for (int64_t i = 0; i < count;) {
         const int64_t src = offset + i, r = src / e.cols, c = src % e.cols;
-        const int64_t dr = (r / 64) * 128 + e.interleave_off + r % 64;
+        const int64_t dr = e.perm.dst(int(r));
         const int64_t take = std::min<int64_t>(count - i, e.cols - c);
         CK(cudaMemcpy(row.data(), static_cast<uint16_t*>(e.ptr) + dr * e.cols + c, 2 * take, cudaMemcpyDeviceToHost));
         for (int64_t k = 0; k < take; ++k) {
@@ -1219,6 +1179,16 @@ int ps_profile_decode(ps_handle* h, int32_t steps, double* ms_out, double* bytes
     }
   }
   CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_trace(ps_handle* h, uint64_t* out, int64_t cap, int32_t* nphases, int32_t* ctas) {
+  if (!h || !nphases || !ctas) return fail(PS_ERR_INVALID, "null argument");
+  if (!h->mega_trace) return fail(PS_ERR_INVALID, "tracing is off (set PS_TRACE=1 before ps_create)");
+  *nphases = 3 + 5 * h->L;
+  *ctas = h->sms;
+  const int64_t n = int64_t(*nphases) * h->sms * 12;
+  if (out) CK(cudaMemcpy(out, h->mega_trace, sizeof(uint64_t) * std::min<int64_t>(cap, n), cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 
