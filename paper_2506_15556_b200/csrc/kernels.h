@@ -205,7 +205,7 @@ struct MegaParams {
   int* am_idx;
   unsigned long long* keys;
   unsigned* bar;            // grid barrier counter, zeroed before launch
-  unsigned long long* trace;  // optional [nphases][G][4] globaltimer stamps
+  unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
 };
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);

@@ -76,6 +76,14 @@ __device__ __forceinline__ void grid_arrive(unsigned* bar) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
 }
 
+// Spin with relaxed loads (an acquire load would invalidate L1 on every
+// iteration), then one acquire fence once the target is reached.
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
   while (ld_acquire_gpu(bar) < target) {
   }
@@ -220,9 +228,16 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
       if (lane == 0) es.rstd[t] = __ldcg(P.rstd0 + t);
     } else {
       // 4 quadrant partials per tile; lane sums entries lane, lane+32, ... in order
-      const int nparts = 4 * ntiles;
+      const int nparts = 4 * ntiles;  // <= 4 * 64
+      float vals[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u;
+        vals[u] = e < nparts ? __ldcg(P.ssq_part + size_t(e) * kMaxWindow + t) : 0.f;
+      }
       float a = 0.f;
-      for (int e = lane; e < nparts; e += 32) a += __ldcg(P.ssq_part + size_t(e) * kMaxWindow + t);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += vals[u];
       const float ssq = warp_sum(a);
       if (lane == 0) es.rstd[t] = 1.0f / sqrtf(ssq / float(P.H) + P.eps);
     }
@@ -237,34 +252,67 @@ constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV pag
 // P.V; the last page to finish for a (row, kv head) merges all pages in page
 // order. The per-(row, head) arithmetic does not depend on the block/pass.
 __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, int t0, int t1, int kvh, int s, int n0, float* sm,
-                               int w, int lane, int* rflag) {
+                               int w, int lane, int* rflag, int trace_p = -1) {
+  const bool tr = trace_p >= 0 && threadIdx.x == 64;
   const int hd = P.hd, grp = P.heads / P.kv_heads;
   const int kmax = min(kPage, n0 + t1 - 1 + 1 - s * kPage);  // keys needed by the last row of the block
   float* Ks = sm;                     // [64][hd+1]
   float* Vs = Ks + kPage * (hd + 1);  // [64][hd], 16-byte aligned rows
   float* Qs = Vs + kPage * hd;        // [kAttnRows][grp][hd]
+  float* Ps = Qs + kAttnRows * grp * hd;  // [4 warps][64] softmax numerators
   const int tid = threadIdx.x - 64;
   const size_t page = size_t(P.page_table[s]);
   const size_t off = size_t(layer) * P.g.layer_stride() + (page * P.kv_heads + kvh) * kPage * hd;
+  // all K/V (and Q) loads of the unit in flight before any is consumed
   const int vpr = hd / 8;
-  for (int e = tid; e < kmax * vpr; e += kWorkers) {
-    const int j = e / vpr, d0 = (e % vpr) * 8;
-    const uint4 kr = __ldcg(reinterpret_cast<const uint4*>(P.kpool + off + size_t(j) * hd + d0));
-    const uint4 vr = __ldcg(reinterpret_cast<const uint4*>(P.vpool + off + size_t(j) * hd + d0));
-    const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kr);
-    const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vr);
+  const int nvec = kmax * vpr;  // <= 64 * 16 = 1024 -> <= 8 per thread
+  uint4 kr[8], vr[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      Ks[j * (hd + 1) + d0 + i] = __bfloat162float(kb[i]);
-      Vs[j * hd + d0 + i] = __bfloat162float(vb[i]);
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + u * kWorkers;
+    if (e < nvec) {
+      const int j = e / vpr, d0 = (e % vpr) * 8;
+      kr[u] = __ldcg(reinterpret_cast<const uint4*>(P.kpool + off + size_t(j) * hd + d0));
+      vr[u] = __ldcg(reinterpret_cast<const uint4*>(P.vpool + off + size_t(j) * hd + d0));
     }
   }
   const int nrows = t1 - t0;
-  for (int e = tid; e < nrows * grp * hd; e += kWorkers) {
-    const int r = e / (grp * hd), rem = e % (grp * hd);
-    Qs[e] = __bfloat162float(__ldcg(P.q + size_t(t0 + r) * P.qd + size_t(kvh) * grp * hd + rem));
+  const int qvec_row = grp * hd / 8;   // uint4 per row of the group's q heads
+  const int nq = nrows * qvec_row;     // <= 4 * 8 * 128 / 8 = 512 -> <= 4 per thread
+  uint4 qr[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * kWorkers;
+    if (e < nq) {
+      const int r = e / qvec_row, rem = (e % qvec_row) * 8;
+      qr[u] = __ldcg(reinterpret_cast<const uint4*>(P.q + size_t(t0 + r) * P.qd + size_t(kvh) * grp * hd + rem));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + u * kWorkers;
+    if (e < nvec) {
+      const int j = e / vpr, d0 = (e % vpr) * 8;
+      const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kr[u]);
+      const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vr[u]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        Ks[j * (hd + 1) + d0 + i] = __bfloat162float(kb[i]);
+        Vs[j * hd + d0 + i] = __bfloat162float(vb[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * kWorkers;
+    if (e < nq) {
+      const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(&qr[u]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Qs[e * 8 + i] = __bfloat162float(qb[i]);
+    }
   }
   wk_bar();
+  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
   for (int pr = w; pr < nrows * grp; pr += 4) {
     const int r = pr / grp, hh = pr % grp;
     const int t = t0 + r, pos = n0 + t;
@@ -272,46 +320,69 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
     const int nkeys = min(kPage, pos + 1 - s * kPage);
     const int h = kvh * grp + hh;
     const float* qs = Qs + (r * grp + hh) * hd;
-    float sc[2];
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int j = lane + 32 * rr;
-      sc[rr] = -INFINITY;
-      if (j < nkeys) {
-        const float* kr = Ks + j * (hd + 1);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 independent chains
-        for (int d = 0; d < hd; d += 4) {
-          a0 = fmaf(qs[d], kr[d], a0);
-          a1 = fmaf(qs[d + 1], kr[d + 1], a1);
-          a2 = fmaf(qs[d + 2], kr[d + 2], a2);
-          a3 = fmaf(qs[d + 3], kr[d + 3], a3);
-        }
-        sc[rr] = ((a0 + a1) + (a2 + a3)) * P.attn_scale;
-      }
+    // scores: lane owns keys lane and lane+32; 8 independent FMA chains
+    const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
+    const float* k0 = Ks + (has0 ? lane : 0) * (hd + 1);
+    const float* k1 = Ks + (has1 ? lane + 32 : 0) * (hd + 1);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < hd; d += 4) {
+      const float4 qv = *reinterpret_cast<const float4*>(qs + d);
+      a0 = fmaf(qv.x, k0[d], a0);
+      a1 = fmaf(qv.y, k0[d + 1], a1);
+      a2 = fmaf(qv.z, k0[d + 2], a2);
+      a3 = fmaf(qv.w, k0[d + 3], a3);
+      b0 = fmaf(qv.x, k1[d], b0);
+      b1 = fmaf(qv.y, k1[d + 1], b1);
+      b2 = fmaf(qv.z, k1[d + 2], b2);
+      b3 = fmaf(qv.w, k1[d + 3], b3);
     }
-    const float mx = warp_max(fmaxf(sc[0], sc[1]));
-    const float p0 = (lane < nkeys) ? expf(sc[0] - mx) : 0.f;
-    const float p1 = (lane + 32 < nkeys) ? expf(sc[1] - mx) : 0.f;
+    const float s0 = has0 ? ((a0 + a1) + (a2 + a3)) * P.attn_scale : -INFINITY;
+    const float s1 = has1 ? ((b0 + b1) + (b2 + b3)) * P.attn_scale : -INFINITY;
+    const float mx = warp_max(fmaxf(s0, s1));
+    const float p0 = has0 ? expf(s0 - mx) : 0.f;
+    const float p1 = has1 ? expf(s1 - mx) : 0.f;
     const float l = warp_sum(p0 + p1);
+    float* Pw = Ps + w * kPage;  // this warp's probabilities
+    Pw[lane] = p0;
+    Pw[lane + 32] = p1;
+    __syncwarp();
     const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
     for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int j = 0; j < nkeys; ++j) {
-        const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
-        const float4 vv = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
-        acc.x = fmaf(pj, vv.x, acc.x);
-        acc.y = fmaf(pj, vv.y, acc.y);
-        acc.z = fmaf(pj, vv.z, acc.z);
-        acc.w = fmaf(pj, vv.w, acc.w);
+      // 4 independent accumulator sets over keys j = 4i + {0,1,2,3}, summed in a fixed order
+      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0, c2 = c0, c3 = c0;
+      const int nk4 = nkeys & ~3;
+      for (int j = 0; j < nk4; j += 4) {
+        const float4 pj = *reinterpret_cast<const float4*>(Pw + j);
+        const float4 v0 = *reinterpret_cast<const float4*>(Vs + (j + 0) * hd + d4);
+        const float4 v1 = *reinterpret_cast<const float4*>(Vs + (j + 1) * hd + d4);
+        const float4 v2 = *reinterpret_cast<const float4*>(Vs + (j + 2) * hd + d4);
+        const float4 v3 = *reinterpret_cast<const float4*>(Vs + (j + 3) * hd + d4);
+        c0.x = fmaf(pj.x, v0.x, c0.x); c0.y = fmaf(pj.x, v0.y, c0.y); c0.z = fmaf(pj.x, v0.z, c0.z); c0.w = fmaf(pj.x, v0.w, c0.w);
+        c1.x = fmaf(pj.y, v1.x, c1.x); c1.y = fmaf(pj.y, v1.y, c1.y); c1.z = fmaf(pj.y, v1.z, c1.z); c1.w = fmaf(pj.y, v1.w, c1.w);
+        c2.x = fmaf(pj.z, v2.x, c2.x); c2.y = fmaf(pj.z, v2.y, c2.y); c2.z = fmaf(pj.z, v2.z, c2.z); c2.w = fmaf(pj.z, v2.w, c2.w);
+        c3.x = fmaf(pj.w, v3.x, c3.x); c3.y = fmaf(pj.w, v3.y, c3.y); c3.z = fmaf(pj.w, v3.z, c3.z); c3.w = fmaf(pj.w, v3.w, c3.w);
       }
+      for (int j = nk4; j < nkeys; ++j) {
+        const float pj = Pw[j];
+        const float4 v0 = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
+        c0.x = fmaf(pj, v0.x, c0.x); c0.y = fmaf(pj, v0.y, c0.y); c0.z = fmaf(pj, v0.z, c0.z); c0.w = fmaf(pj, v0.w, c0.w);
+      }
+      float4 acc;
+      acc.x = (c0.x + c1.x) + (c2.x + c3.x);
+      acc.y = (c0.y + c1.y) + (c2.y + c3.y);
+      acc.z = (c0.z + c1.z) + (c2.z + c3.z);
+      acc.w = (c0.w + c1.w) + (c2.w + c3.w);
       *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc;
     }
+    __syncwarp();
     if (lane == 0) {
       P.ml_part[slot * 2] = mx;
       P.ml_part[slot * 2 + 1] = l;
     }
   }
   wk_bar();
+  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 9);
   // page arrival for every row of the block at once; the last page merges
   if (tid < nrows) {
     const int t = t0 + tid, pos = n0 + t;
@@ -326,6 +397,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
     }
   }
   wk_bar();
+  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
   for (int r = 0; r < nrows; ++r) {
     if (!rflag[r]) continue;
     const int t = t0 + r, pos = n0 + t;
@@ -361,6 +433,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
     }
   }
   wk_bar();
+  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
 }
 
 // Sum a split tile's piece partials (in CTA order, all loads in flight) for
@@ -444,10 +517,17 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
 
   if (warp == 0) {
     // ======================= TMA producer =======================
+    // Weight tiles of a phase are issued into the ring before waiting for the
+    // barrier that guards its activations; weights stream with an L2
+    // evict-first policy (read once per pass) so activations, KV pages and
+    // split-K partials stay L2-resident. (A TMA L2-prefetch cursor running
+    // further ahead was measured slower: prefetched lines were evicted before
+    // use and DRAM traffic grew 1.8x — see DESIGN.md.)
     if (lane == 0) {
       grid_wait(P.bar, unsigned(G));  // embed done (and the stop flag settled)
       if (!P.ctx->stop) {
         const int xrow_lm = n0;
+        const uint64_t pol_stream = l2_policy_evict_first();
         uint32_t it = 0;
         for (int p = 1; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
@@ -465,7 +545,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
             const int x = kb_lo + i, tile = x / g.KB, kb = x % g.KB;
-            tma_load_2d(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128);
+            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
           }
           grid_wait(P.bar, unsigned(G) * unsigned(p));  // activations of this phase are complete
           stamp(P, p, c, G, 0);
@@ -480,7 +560,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
             const int x = kb_lo + i, tile = x / g.KB, kb = x % g.KB;
-            tma_load_2d(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128);
+            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
             tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
           }
           it += nk;
@@ -590,8 +670,16 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         for (int t = c * 4 + w; t < rows; t += 4 * G) {
           float bv = -INFINITY;
           int bi = 0x7fffffff;
-          for (int cc = lane; cc < G; cc += 32)
-            argmax_merge(bv, bi, __ldcg(P.am_val + size_t(cc) * kMaxWindow + t), __ldcg(P.am_idx + size_t(cc) * kMaxWindow + t));
+          float vv[8];
+          int ii[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {  // G <= 256
+            const int cc = lane + 32 * u;
+            vv[u] = cc < G ? __ldcg(P.am_val + size_t(cc) * kMaxWindow + t) : -INFINITY;
+            ii[u] = cc < G ? __ldcg(P.am_idx + size_t(cc) * kMaxWindow + t) : 0x7fffffff;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) argmax_merge(bv, bi, vv[u], ii[u]);
           warp_argmax(bv, bi);
           if (lane == 0) {
             P.argmax_pos[n0 + t] = bi;
@@ -610,12 +698,15 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         const int npages = (n0 + rows - 1) / kPage + 1;
         const int nblocks = (rows + kAttnRows - 1) / kAttnRows;
         const int units = nblocks * P.kv_heads * npages;
+        bool first_unit = true;
         for (int u = c; u < units; u += G) {
           const int s = u % npages, r = u / npages;
           const int kvh = r % P.kv_heads, blk = r / P.kv_heads;
           const int t0 = blk * kAttnRows, t1 = min(rows, t0 + kAttnRows);
           if (s > (n0 + t1 - 1) / kPage) continue;  // no row of the block reaches this page
-          attention_unit(P, layer, t0, t1, kvh, s, n0, attn_sm, w, lane, es.rflag);
+          if (tid == 0 && first_unit) stamp(P, p, c, G, 7);
+          attention_unit(P, layer, t0, t1, kvh, s, n0, attn_sm, w, lane, es.rflag, first_unit ? p : -1);
+          first_unit = false;
         }
       } else {
         if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {
@@ -684,10 +775,10 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
               es.flag = old == unsigned(npieces - 1);
             }
             wk_bar();
-            if (spread) {
+            // finalisation is deferred until all of this CTA's pieces are
+            // published, so a tile's finaliser never delays the next tile's piece
+            if (spread || es.flag) {
               if (dtile0 < 0) dtile0 = tile; else dtile1 = tile;
-            } else if (es.flag) {
-              finish_from_pieces(P, kind, layer, 0, rows, n0, tile, m, q, lane, c_first, npieces, g, es);
             }
           }
           ++acc_it;
@@ -700,12 +791,17 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           if (tile < 0) continue;
           const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
           const int npieces = c_last - c_first + 1, my_idx = c - c_first;
-          const int r_lo = my_idx * rows / npieces, r_hi = (my_idx + 1) * rows / npieces;
-          if (tid == 0) {
-            grid_wait(cnt + tile, unsigned(npieces));
-            if (d == 0) stamp(P, p, c, G, 7);
+          // spread: every piece's CTA takes a share of the rows; otherwise this
+          // CTA was the last arrival and finalises all rows
+          const int r_lo = spread ? my_idx * rows / npieces : 0;
+          const int r_hi = spread ? (my_idx + 1) * rows / npieces : rows;
+          if (spread) {
+            if (tid == 0) {
+              grid_wait(cnt + tile, unsigned(npieces));
+              if (d == 0) stamp(P, p, c, G, 7);
+            }
+            wk_bar();
           }
-          wk_bar();
           if (r_lo < r_hi) finish_from_pieces(P, kind, layer, r_lo, r_hi, n0, tile, m, q, lane, c_first, npieces, g, es);
         }
         if (tid == 0) stamp(P, p, c, G, 6);

@@ -33,7 +33,7 @@ def report(tr, label):
         start = np.nanmax(tr[p - 1, :, 2])
         a = agg[names[p]]
         a["span"].append(np.nanmax(tr[p, :, 2]) - start)
-        for slot, key in ((1, "bar"), (4, "acc_last"), (5, "published"), (7, "waited"), (8, "fin0_start"), (9, "fin0_loaded"), (10, "fin0_done"), (6, "deferred")):
+        for slot, key in ((1, "bar"), (4, "acc_last"), (5, "published"), (7, "waited|a_start"), (8, "a_loaded"), (9, "a_computed"), (10, "a_counted"), (11, "a_merged"), (6, "deferred")):
             col = tr[p, :, slot]
             if np.isfinite(col).any():
                 a[key + "_max"].append(np.nanmax(col) - start)
@@ -47,3 +47,13 @@ lm.discard_after(len(toks) - 8)
 v = lm.verify_greedy_detail(toks, [5] * 64)
 print("verify gpu ms", v["gpu_ms"])
 report(grab(), "verify")
+# per-CTA straggler view of the decode step (slot 4 = last accumulator seen)
+lm.discard_after(len(toks))
+lm.decode_greedy_fused(toks, 2)
+tr = grab()
+for p in (6, 8, 9, 10):  # layer-1 QKV, O, GU, D
+    start = np.nanmax(tr[p - 1, :, 2])
+    acc = tr[p, :, 4] - start
+    order = np.argsort(-np.nan_to_num(acc, nan=-1))
+    print(names[p], "slowest CTAs", [(int(i), round(float(acc[i]), 1)) for i in order[:10]],
+          "median", round(float(np.nanmedian(acc)), 1))
