@@ -119,7 +119,9 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    # PS_BENCH_SHARE_GPU=1: every rank on device 0 (tests the N>1 path on one GPU)
+    device = 0 if os.environ.get("PS_BENCH_SHARE_GPU") == "1" else local
+    return world, rank, device
 
 
 def cpu_port_timing(shape, sample_s: float, threads: int, context: int = 128, window: int = 72) -> dict:
@@ -200,8 +202,11 @@ def main():
     import torch
     torch.cuda.set_device(local)
     if world > 1:
+        # The conversation shards never exchange data; the only collectives are
+        # the timing barrier and a max over two scalars, so gloo (host) is used
+        # and NCCL stays off the data path.
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
     from paper_2506_15556_b200 import B200LM, summarize_percentiles
     from paper_2506_15556_b200.shapes import SHAPES
     from paper_2506_15556_b200.workload import WorkloadSpec, c5_config, shard, simulate, synthetic_conversations
@@ -256,7 +261,7 @@ def main():
     verify_nonzero = [x for x in lm.verify_ms if x > 0]
     vals = {"elapsed": elapsed_ms, "device": device_ms}
     if world > 1:
-        t = torch.tensor([elapsed_ms, device_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([elapsed_ms, device_ms], dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         vals = {"elapsed": float(t[0]), "device": float(t[1])}
     # roofline of the dominant kernel class, CUDA events around every launch
@@ -281,7 +286,8 @@ def main():
     line = {
         "metric": METRIC, "value": world * n_conv / (vals["device"] / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": vals["elapsed"] / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if shape.mode == 1 else "f32",
         "data": "synthetic (random-init weights, synthetic vocabulary and conversations)",
         "config": {"workload": "c5: synthetic MT-Bench/Lmsys-length conversations, Llama-3-8B shape, bf16, "
                                "measured-cost SimClock", "shape": shape.name, "conversations_per_rank_per_step": per,

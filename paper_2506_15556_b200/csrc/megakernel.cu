@@ -59,6 +59,19 @@ __device__ __forceinline__ int sk_start(int c, int G, int T) { return (c * T) / 
 // CTA whose k-block range contains global block x
 __device__ __forceinline__ int sk_owner(int x, int G, int T) { return ((x + 1) * G + T - 1) / T - 1; }
 
+// A CTA's k-blocks in order, one piece per tile touched (the natural order
+// keeps DRAM access sequential; finishing order was measured not to matter).
+struct PieceOrder {
+  int lo, hi, KB, t_first;
+  __device__ __forceinline__ PieceOrder(int lo_, int hi_, int KB_) : lo(lo_), hi(hi_), KB(KB_), t_first(lo_ / KB_) {}
+  __device__ __forceinline__ int npieces() const { return hi > lo ? (hi - 1) / KB - t_first + 1 : 0; }
+  __device__ __forceinline__ int block(int i) const { return lo + i; }
+  __device__ __forceinline__ void piece(int j, int& plo, int& phi) const {
+    plo = max(lo, (t_first + j) * KB);
+    phi = min(hi, (t_first + j + 1) * KB);
+  }
+};
+
 // atomic add with acquire+release at GPU scope: orders this CTA's prior
 // writes (made visible to thread 0 by the preceding bar.sync) before the
 // counter update, and the finalizer's later reads after it.
@@ -148,6 +161,15 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     const int dim = even ? pi : pi + half;  // dimension within the head
     const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
     const float bias = P.qkv_bias ? __bfloat162float(P.qkv_bias[size_t(layer) * (P.qd + 2 * P.kvd) + n]) : 0.f;
+    // every global load of the chunk first (no aliasing with the stores below)
+    float2 cs[8];
+    int page[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = c0 + j, pos = n0 + t;
+      cs[j] = (t < rows && (is_q || is_k)) ? __ldg(P.rope + size_t(pos) * half + pi) : make_float2(1.f, 0.f);
+      page[j] = (t < rows && !is_q) ? __ldg(P.page_table + pos / kPage) : 0;
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int t = c0 + j;
@@ -157,10 +179,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       if (!valid) continue;
       const int pos = n0 + t;
       float out = val;
-      if (is_q || is_k) {
-        const float2 cs = P.rope[size_t(pos) * half + pi];
-        out = even ? val * cs.x - other * cs.y : val * cs.x + other * cs.y;
-      }
+      if (is_q || is_k) out = even ? val * cs[j].x - other * cs[j].y : val * cs[j].x + other * cs[j].y;
       const __nv_bfloat16 ob = __float2bfloat16_rn(out);
       const int col = n - r + dim;  // original (unpermuted) output column
       if (is_q) {
@@ -168,9 +187,8 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       } else {
         const int cc = col - P.qd - (is_k ? 0 : P.kvd);
         const int h = cc / hd;
-        const size_t page = size_t(P.page_table[pos / kPage]);
         const size_t off = size_t(layer) * P.g.layer_stride() +
-                           ((page * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc % hd);
+                           ((size_t(page[j]) * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc % hd);
         (is_k ? P.kpool : P.vpool)[off] = ob;
       }
     }
@@ -185,13 +203,16 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
+    float xo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xo[j] = (c0 + j < rows) ? __ldcg(P.x + size_t(c0 + j) * P.H + n) : 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int t = c0 + j;
       float sq = 0.f;
       if (t < rows) {
         float* xp = P.x + size_t(t) * P.H + n;
-        const float xi = *xp + v[j];
+        const float xi = xo[j] + v[j];
         *xp = xi;
         __nv_bfloat16* dst = to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H;
         dst[n] = __float2bfloat16_rn(xi);
@@ -259,7 +280,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
   float* Ks = sm;                     // [64][hd+1]
   float* Vs = Ks + kPage * (hd + 1);  // [64][hd], 16-byte aligned rows
   float* Qs = Vs + kPage * hd;        // [kAttnRows][grp][hd]
-  float* Ps = Qs + kAttnRows * grp * hd;  // [4 warps][64] softmax numerators
+  float* Ps = Qs + kAttnRows * grp * hd;  // [4 warps][4 heads][64] softmax numerators
   const int tid = threadIdx.x - 64;
   const size_t page = size_t(P.page_table[s]);
   const size_t off = size_t(layer) * P.g.layer_stride() + (page * P.kv_heads + kvh) * kPage * hd;
@@ -313,72 +334,85 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
   }
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
-  for (int pr = w; pr < nrows * grp; pr += 4) {
-    const int r = pr / grp, hh = pr % grp;
+  // One warp per query row, all heads of the GQA group (<= 4 at a time):
+  // every K/V element read from shared memory feeds 4 heads -> 16 independent
+  // FMA chains per lane. Scores: lane owns keys lane and lane+32.
+  for (int r = w; r < nrows; r += 4) {
     const int t = t0 + r, pos = n0 + t;
     if (s > pos / kPage) continue;  // this page is beyond the row's causal range
     const int nkeys = min(kPage, pos + 1 - s * kPage);
-    const int h = kvh * grp + hh;
-    const float* qs = Qs + (r * grp + hh) * hd;
-    // scores: lane owns keys lane and lane+32; 8 independent FMA chains
     const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
     const float* k0 = Ks + (has0 ? lane : 0) * (hd + 1);
     const float* k1 = Ks + (has1 ? lane + 32 : 0) * (hd + 1);
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
-#pragma unroll 4
-    for (int d = 0; d < hd; d += 4) {
-      const float4 qv = *reinterpret_cast<const float4*>(qs + d);
-      a0 = fmaf(qv.x, k0[d], a0);
-      a1 = fmaf(qv.y, k0[d + 1], a1);
-      a2 = fmaf(qv.z, k0[d + 2], a2);
-      a3 = fmaf(qv.w, k0[d + 3], a3);
-      b0 = fmaf(qv.x, k1[d], b0);
-      b1 = fmaf(qv.y, k1[d + 1], b1);
-      b2 = fmaf(qv.z, k1[d + 2], b2);
-      b3 = fmaf(qv.w, k1[d + 3], b3);
-    }
-    const float s0 = has0 ? ((a0 + a1) + (a2 + a3)) * P.attn_scale : -INFINITY;
-    const float s1 = has1 ? ((b0 + b1) + (b2 + b3)) * P.attn_scale : -INFINITY;
-    const float mx = warp_max(fmaxf(s0, s1));
-    const float p0 = has0 ? expf(s0 - mx) : 0.f;
-    const float p1 = has1 ? expf(s1 - mx) : 0.f;
-    const float l = warp_sum(p0 + p1);
-    float* Pw = Ps + w * kPage;  // this warp's probabilities
-    Pw[lane] = p0;
-    Pw[lane + 32] = p1;
-    __syncwarp();
-    const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-    for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-      // 4 independent accumulator sets over keys j = 4i + {0,1,2,3}, summed in a fixed order
-      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0, c2 = c0, c3 = c0;
-      const int nk4 = nkeys & ~3;
-      for (int j = 0; j < nk4; j += 4) {
-        const float4 pj = *reinterpret_cast<const float4*>(Pw + j);
-        const float4 v0 = *reinterpret_cast<const float4*>(Vs + (j + 0) * hd + d4);
-        const float4 v1 = *reinterpret_cast<const float4*>(Vs + (j + 1) * hd + d4);
-        const float4 v2 = *reinterpret_cast<const float4*>(Vs + (j + 2) * hd + d4);
-        const float4 v3 = *reinterpret_cast<const float4*>(Vs + (j + 3) * hd + d4);
-        c0.x = fmaf(pj.x, v0.x, c0.x); c0.y = fmaf(pj.x, v0.y, c0.y); c0.z = fmaf(pj.x, v0.z, c0.z); c0.w = fmaf(pj.x, v0.w, c0.w);
-        c1.x = fmaf(pj.y, v1.x, c1.x); c1.y = fmaf(pj.y, v1.y, c1.y); c1.z = fmaf(pj.y, v1.z, c1.z); c1.w = fmaf(pj.y, v1.w, c1.w);
-        c2.x = fmaf(pj.z, v2.x, c2.x); c2.y = fmaf(pj.z, v2.y, c2.y); c2.z = fmaf(pj.z, v2.z, c2.z); c2.w = fmaf(pj.z, v2.w, c2.w);
-        c3.x = fmaf(pj.w, v3.x, c3.x); c3.y = fmaf(pj.w, v3.y, c3.y); c3.z = fmaf(pj.w, v3.z, c3.z); c3.w = fmaf(pj.w, v3.w, c3.w);
+    for (int hb = 0; hb < grp; hb += 4) {
+      const int nhh = min(4, grp - hb);
+      const float* qb = Qs + (r * grp + hb) * hd;
+      float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+      for (int d = 0; d < hd; d += 4) {
+        const float k00 = k0[d], k01 = k0[d + 1], k02 = k0[d + 2], k03 = k0[d + 3];
+        const float k10 = k1[d], k11 = k1[d + 1], k12 = k1[d + 2], k13 = k1[d + 3];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          if (hh < nhh) {
+            const float4 qv = *reinterpret_cast<const float4*>(qb + hh * hd + d);
+            a0[hh] = fmaf(qv.w, k03, fmaf(qv.z, k02, fmaf(qv.y, k01, fmaf(qv.x, k00, a0[hh]))));
+            a1[hh] = fmaf(qv.w, k13, fmaf(qv.z, k12, fmaf(qv.y, k11, fmaf(qv.x, k10, a1[hh]))));
+          }
+        }
       }
-      for (int j = nk4; j < nkeys; ++j) {
-        const float pj = Pw[j];
-        const float4 v0 = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
-        c0.x = fmaf(pj, v0.x, c0.x); c0.y = fmaf(pj, v0.y, c0.y); c0.z = fmaf(pj, v0.z, c0.z); c0.w = fmaf(pj, v0.w, c0.w);
+      float* Pw = Ps + w * 4 * kPage;  // this warp's numerators [4 heads][64 keys]
+      float mxs[4], ls[4];
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        if (hh < nhh) {
+          const float s0 = has0 ? a0[hh] * P.attn_scale : -INFINITY;
+          const float s1 = has1 ? a1[hh] * P.attn_scale : -INFINITY;
+          const float mx = warp_max(fmaxf(s0, s1));
+          const float p0 = has0 ? expf(s0 - mx) : 0.f;
+          const float p1 = has1 ? expf(s1 - mx) : 0.f;
+          ls[hh] = warp_sum(p0 + p1);
+          mxs[hh] = mx;
+          Pw[hh * kPage + lane] = p0;
+          Pw[hh * kPage + lane + 32] = p1;
+        }
       }
-      float4 acc;
-      acc.x = (c0.x + c1.x) + (c2.x + c3.x);
-      acc.y = (c0.y + c1.y) + (c2.y + c3.y);
-      acc.z = (c0.z + c1.z) + (c2.z + c3.z);
-      acc.w = (c0.w + c1.w) + (c2.w + c3.w);
-      *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      P.ml_part[slot * 2] = mx;
-      P.ml_part[slot * 2 + 1] = l;
+      __syncwarp();
+      for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+        float4 acc[4];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < nkeys; ++j) {
+          const float4 vv = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh) {
+            const float pj = Pw[hh * kPage + j];
+            acc[hh].x = fmaf(pj, vv.x, acc[hh].x);
+            acc[hh].y = fmaf(pj, vv.y, acc[hh].y);
+            acc[hh].z = fmaf(pj, vv.z, acc[hh].z);
+            acc[hh].w = fmaf(pj, vv.w, acc[hh].w);
+          }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          if (hh < nhh) {
+            const int h = kvh * grp + hb + hh;
+            const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
+            *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc[hh];
+          }
+        }
+      }
+      if (lane < nhh) {
+        const int h = kvh * grp + hb + lane;
+        const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
+        float mxl = mxs[0], ll = ls[0];
+#pragma unroll
+        for (int hh = 1; hh < 4; ++hh)
+          if (lane == hh) { mxl = mxs[hh]; ll = ls[hh]; }
+        P.ml_part[slot * 2] = mxl;
+        P.ml_part[slot * 2 + 1] = ll;
+      }
+      __syncwarp();
     }
   }
   wk_bar();
@@ -535,6 +569,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           const Gemm g = gemm_of(P, kind);
           const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
           const int nk = kb_hi - kb_lo;
+          const PieceOrder po(kb_lo, kb_hi, g.KB);
           const CUtensorMap* wm = wmap_of(P, p, kind);
           const CUtensorMap* xm = xmap_of(P, kind);
           const int xrow = kind == PH_LM ? xrow_lm : 0;
@@ -544,7 +579,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             const uint32_t s = (it + i) % ST, ph = ((it + i) / ST) & 1;
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
-            const int x = kb_lo + i, tile = x / g.KB, kb = x % g.KB;
+            const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
             tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
           }
           grid_wait(P.bar, unsigned(G) * unsigned(p));  // activations of this phase are complete
@@ -552,14 +587,14 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           fence_proxy_async_global();
           for (int i = 0; i < pre; ++i) {
             const uint32_t s = (it + i) % ST;
-            const int x = kb_lo + i, kb = x % g.KB;
+            const int x = po.block(i), kb = x % g.KB;
             tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
           }
           for (int i = pre; i < nk; ++i) {
             const uint32_t s = (it + i) % ST, ph = ((it + i) / ST) & 1;
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
-            const int x = kb_lo + i, tile = x / g.KB, kb = x % g.KB;
+            const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
             tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
             tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
           }
@@ -579,10 +614,10 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           if (kind == PH_ATTN || kind == PH_FINAL) continue;
           const Gemm g = gemm_of(P, kind);
           const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
-          int x = kb_lo;
-          while (x < kb_hi) {  // one piece per tile touched by this CTA
-            const int tile = x / g.KB;
-            const int piece_hi = min(kb_hi, (tile + 1) * g.KB);
+          const PieceOrder po(kb_lo, kb_hi, g.KB);
+          for (int j = 0; j < po.npieces(); ++j) {  // one piece per tile touched by this CTA
+            int x, piece_hi;
+            po.piece(j, x, piece_hi);
             const uint32_t b = acc_it & 1, aph = (acc_it >> 1) & 1;
             mbar_wait(acc_empty0 + 8 * b, aph ^ 1);
             tc_fence_after();
@@ -600,7 +635,6 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             }
             umma_commit(acc_full0 + 8 * b);
             ++acc_it;
-            x = piece_hi;
           }
           stamp(P, p, c, G, 3);
         }
@@ -717,7 +751,6 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         }
         const Gemm g = gemm_of(P, kind);
         const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
-        const int first_tile = kb_lo / g.KB;
         // per-phase arrival counters (zeroed before the pass): no resets, no reuse races
         unsigned* cnt = P.tile_cnt + size_t(p) * P.max_tiles;
         // Few rows (decode): the last piece to arrive finalizes the whole tile.
@@ -732,10 +765,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           }
           wk_bar();
         }
-        int x = kb_lo;
-        while (x < kb_hi) {
+        const PieceOrder po(kb_lo, kb_hi, g.KB);
+        for (int pj = 0; pj < po.npieces(); ++pj) {
+          int x, piece_hi;
+          po.piece(pj, x, piece_hi);
           const int tile = x / g.KB;
-          const int piece_hi = min(kb_hi, (tile + 1) * g.KB);
           const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
           const int npieces = c_last - c_first + 1;  // <= 8 by the choice of g.G
           {
@@ -782,7 +816,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             }
           }
           ++acc_it;
-          x = piece_hi;
+          (void)piece_hi;
         }
         if (tid == 0) stamp(P, p, c, G, 5);
         // second pass (many rows): wait for each split tile's pieces, finalize this CTA's row share
@@ -832,12 +866,27 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   }
 }
 
-int mega_stages(int ntok, int attn_floats) {
+int mega_static_smem() {
   static int static_smem = -1;
   if (static_smem < 0) {
     cudaFuncAttributes fa{};
     static_smem = cudaFuncGetAttributes(&fa, mega_kernel) == cudaSuccess ? int(fa.sharedSizeBytes) : 16 * 1024;
   }
+  return static_smem;
+}
+
+// One fixed attribute (the most any pass width may use), set once, so
+// handles created later never shrink it under a running configuration.
+cudaError_t mega_set_smem_attr() {
+  static cudaError_t done = cudaErrorNotReady;
+  if (done == cudaErrorNotReady)
+    done = cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024 - mega_static_smem());
+  return done;
+}
+
+int mega_stages(int ntok, int attn_floats) {
+  const int static_smem = mega_static_smem();
   const int stage = kTileABytes + ntok * 128;
   // 227 KB per CTA minus static shared memory, attention staging and the
   // 1 KB alignment slack
@@ -851,12 +900,7 @@ int mega_smem_bytes(int ntok, int stages, int attn_floats) {
 }
 
 cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st) {
-  static int attr_smem = -1;
-  if (attr_smem != smem) {
-    const cudaError_t e = cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_smem = smem;
-  }
+  if (const cudaError_t e = mega_set_smem_attr(); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(192);
@@ -871,7 +915,7 @@ cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st
 }
 
 int mega_max_blocks_per_sm(int smem) {
-  if (cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+  if (mega_set_smem_attr() != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel, 192, smem) != cudaSuccess) return 0;
   return n;
