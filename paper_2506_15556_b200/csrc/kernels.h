@@ -197,7 +197,8 @@ struct MegaParams {
   float* o_part;
   float* ml_part;
   unsigned* acnt;
-  float* part;              // [G][2][kMaxWindow][128] stream-K piece partials
+  float* part;              // [G][2][kMaxWindow][128] stream-K piece partials (u64 tagged for <= 8 rows)
+  unsigned* epoch;          // pass counter (partial tags), advanced by CTA 0 at the end of each pass
   unsigned* tile_cnt;       // [phase][max_tiles], zeroed before the pass
   int max_tiles;
   unsigned* lm_cnt;

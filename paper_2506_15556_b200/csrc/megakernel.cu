@@ -151,8 +151,10 @@ struct EpiSmem {
 // are adjacent rows (RowPerm kHeadPairs / kGateUp) -> one shuffle; row sums
 // (sum of squares, argmax) stay per warp quadrant and are combined by their
 // consumer in a fixed order.
+// NR: rows the call site can have in this chunk (8, or 1 for the decode finaliser).
+template <int NR = 8>
 __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows, int n0, int tile, int m, int q,
-                             int lane, int c0, const float (&v)[8], EpiSmem& es) {
+                             int lane, int c0, const float (&v)[8], EpiSmem& es, const float* xo_pre = nullptr) {
   const int n = tile * 128 + m;
   if (kind == PH_QKV) {
     const int hd = P.hd, half = hd >> 1;
@@ -162,16 +164,16 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
     const float bias = P.qkv_bias ? __bfloat162float(P.qkv_bias[size_t(layer) * (P.qd + 2 * P.kvd) + n]) : 0.f;
     // every global load of the chunk first (no aliasing with the stores below)
-    float2 cs[8];
-    int page[8];
+    float2 cs[NR];
+    int page[NR];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const int t = c0 + j, pos = n0 + t;
       cs[j] = (t < rows && (is_q || is_k)) ? __ldg(P.rope + size_t(pos) * half + pi) : make_float2(1.f, 0.f);
       page[j] = (t < rows && !is_q) ? __ldg(P.page_table + pos / kPage) : 0;
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
       const bool valid = t < rows;
       const float val = valid ? v[j] * es.rstd[t] + bias : 0.f;
@@ -194,7 +196,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     }
   } else if (kind == PH_GU) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
       const float val = t < rows ? v[j] * es.rstd[t] : 0.f;
       const float up = __shfl_xor_sync(0xffffffffu, val, 1);
@@ -203,11 +205,12 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
-    float xo[8];
+    float xo[NR];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) xo[j] = (c0 + j < rows) ? __ldcg(P.x + size_t(c0 + j) * P.H + n) : 0.f;
+    for (int j = 0; j < NR; ++j)
+      xo[j] = xo_pre ? xo_pre[j] : (c0 + j < rows) ? __ldcg(P.x + size_t(c0 + j) * P.H + n) : 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
       float sq = 0.f;
       if (t < rows) {
@@ -226,7 +229,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     const int vid = P.v_begin + n;
     const float b = valid ? P.lm_bias[vid] : 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
       float lv = -INFINITY;
       int li = 0x7fffffff;
@@ -334,18 +337,25 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
   }
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
-  // One warp per query row, all heads of the GQA group (<= 4 at a time):
-  // every K/V element read from shared memory feeds 4 heads -> 16 independent
-  // FMA chains per lane. Scores: lane owns keys lane and lane+32.
-  for (int r = w; r < nrows; r += 4) {
+  // Work item = (query row, slice of the GQA group's heads), one per warp,
+  // each (row, head) computed identically whatever the slicing: with >= 4 rows
+  // a warp takes a row and all its heads (<= 4 at a time, every K/V element
+  // read from shared memory feeds 4 heads -> 16 FMA chains per lane); with
+  // fewer rows (decode) the heads are spread over the warps. Scores: lane
+  // owns keys lane and lane+32.
+  const int warps_per_row = nrows >= 4 ? 1 : 4 / nrows;
+  const int hs = (grp + warps_per_row - 1) / warps_per_row;
+  const int nchunk = (grp + hs - 1) / hs;
+  for (int item = w; item < nrows * nchunk; item += 4) {
+    const int r = item / nchunk, h_lo = (item % nchunk) * hs, h_hi = min(grp, h_lo + hs);
     const int t = t0 + r, pos = n0 + t;
     if (s > pos / kPage) continue;  // this page is beyond the row's causal range
     const int nkeys = min(kPage, pos + 1 - s * kPage);
     const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
     const float* k0 = Ks + (has0 ? lane : 0) * (hd + 1);
     const float* k1 = Ks + (has1 ? lane + 32 : 0) * (hd + 1);
-    for (int hb = 0; hb < grp; hb += 4) {
-      const int nhh = min(4, grp - hb);
+    for (int hb = h_lo; hb < h_hi; hb += 4) {
+      const int nhh = min(4, h_hi - hb);
       const float* qb = Qs + (r * grp + hb) * hd;
       float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2
@@ -470,11 +480,57 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
 }
 
-// Sum a split tile's piece partials (in CTA order, all loads in flight) for
-// rows [r_lo, r_hi) and run the phase's finishing math on them.
 // Partial slot of CTA cc's piece of `tile` (slot 0 = the CTA's first tile).
 __device__ __forceinline__ int piece_off(int cc, int tile, const Gemm& g, int m) {
   return (cc * 2 + (sk_start(cc, g.G, g.T) / g.KB == tile ? 0 : 1)) * kMaxWindow * 128 + m;
+}
+
+// Few-row passes (decode): a piece's partial is published as one 64-bit
+// relaxed store of (tag, fp32 bits) — single-copy atomic, so a reader that sees
+// the pass/phase tag sees the value, with no fence or arrival counter on the
+// writer's side. The tile's finaliser is fixed: the CTA holding the tile's
+// first k-block (for it that piece is the last of its range, so it finishes
+// last) — it adds its own accumulator from registers and polls the others.
+__device__ __forceinline__ void st_tagged(unsigned long long* p, unsigned tag, float v) {
+  const unsigned long long w = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+// Finaliser of a split tile in a 1-row pass (decode): own partial (CTA
+// c_first) plus the tagged partials of CTAs c_first+1 .. c_first+npieces-1,
+// summed in CTA order (the order of finish_from_pieces), then the phase's
+// finishing math. The O/D residual load is issued with the partial loads.
+__device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int layer, int n0, int tile, int m, int q,
+                                              int lane, int c_first, int npieces, const Gemm& g, unsigned tag, float own,
+                                              EpiSmem& es) {
+  const unsigned long long* part = reinterpret_cast<const unsigned long long*>(P.part);
+  const bool resid = kind == PH_O || kind == PH_D;
+  float xo[1] = {resid ? __ldcg(P.x + tile * 128 + m) : 0.f};
+  unsigned long long w[7];
+#pragma unroll
+  for (int pc = 1; pc < 8; ++pc)
+    if (pc < npieces) w[pc - 1] = ld_tagged(part + piece_off(c_first + pc, tile, g, m));
+  bool again = true;
+  while (again) {
+    again = false;
+#pragma unroll
+    for (int pc = 1; pc < 8; ++pc)
+      if (pc < npieces && unsigned(w[pc - 1] >> 32) != tag) {
+        w[pc - 1] = ld_tagged(part + piece_off(c_first + pc, tile, g, m));
+        again = true;
+      }
+  }
+  float v[8];
+  v[0] = own;
+#pragma unroll
+  for (int pc = 1; pc < 8; ++pc)
+    if (pc < npieces) v[0] += __uint_as_float(unsigned(w[pc - 1]));
+  finish_chunk<1>(P, kind, layer, 1, n0, tile, m, q, lane, 0, v, es, resid ? xo : nullptr);
 }
 
 // Sum a split tile's piece partials (pieces = CTAs c_first.., in CTA order,
@@ -516,6 +572,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x, G = gridDim.x;
   const int ST = P.stages;
+  // partial tags of this pass: epoch * nphases + phase (the epoch advances once per pass)
+  const unsigned epoch = *P.epoch;
+  const unsigned tag0 = epoch * unsigned(3 + 5 * P.L);
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_bytes = P.ntok * 128;
   auto a_tile = [&](int s) { return base + size_t(s) * (kTileABytes + b_bytes); };
@@ -753,10 +812,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         const int kb_lo = c < g.G ? sk_start(c, g.G, g.T) : 0, kb_hi = c < g.G ? sk_start(c + 1, g.G, g.T) : 0;
         // per-phase arrival counters (zeroed before the pass): no resets, no reuse races
         unsigned* cnt = P.tile_cnt + size_t(p) * P.max_tiles;
-        // Few rows (decode): the last piece to arrive finalizes the whole tile.
-        // Many rows (verify/prefill): every piece publishes without blocking,
+        // 1-row pass (decode): pieces publish tagged partials and the tile's
+        // first-block CTA finalizes (finish_tagged). Wider passes (verify /
+        // prefill): every piece publishes without blocking and counts in,
         // then each piece's CTA finalizes its own share of the rows.
-        const bool spread = rows > 8;
+        const bool spread = rows > 1;
         int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
         if (kind == PH_LM) {
           for (int e = tid; e < 4 * kMaxWindow; e += kWorkers) {
@@ -789,6 +849,22 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
               tmem_ld8(trow + c0, v);
               finish_chunk(P, kind, layer, rows, n0, tile, m, q, lane, c0, v, es);
             }
+            tc_fence_before();
+            wk_bar();
+            if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
+          } else if (!spread && c == c_first) {
+            // fixed finaliser (few rows): own accumulator + the other pieces' tagged partials
+            float v[8];
+            tmem_ld8(trow, v);
+            tc_fence_before();
+            wk_bar();
+            if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
+            finish_tagged(P, kind, layer, n0, tile, m, q, lane, c_first, npieces, g, tag0 + unsigned(p), v[0], es);
+          } else if (!spread) {
+            unsigned long long* mine = reinterpret_cast<unsigned long long*>(P.part) + piece_off(c, tile, g, m);
+            float v[8];
+            tmem_ld8(trow, v);
+            st_tagged(mine, tag0 + unsigned(p), v[0]);
             tc_fence_before();
             wk_bar();
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
@@ -836,7 +912,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             }
             wk_bar();
           }
+          if (tid == 0 && d == 0) stamp(P, p, c, G, 8);
           if (r_lo < r_hi) finish_from_pieces(P, kind, layer, r_lo, r_hi, n0, tile, m, q, lane, c_first, npieces, g, es);
+          if (tid == 0 && d == 0) stamp(P, p, c, G, 9);
         }
         if (tid == 0) stamp(P, p, c, G, 6);
         if (kind == PH_LM) {
@@ -860,6 +938,8 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   }
   tc_fence_before();
   __syncthreads();
+  // every CTA read the epoch before the embed barrier, which CTA 0 passed
+  if (c == 0 && threadIdx.x == 0) *P.epoch = epoch + 1;
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * P.acc_cols) : "memory");

@@ -210,6 +210,7 @@ struct ps_handle {
   unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [64..] per-phase tile counters
   int mega_max_tiles = 0;
   size_t mega_cnt_words = 0;
+  unsigned* mega_epoch = nullptr;
   unsigned long long* mega_trace = nullptr;  // PS_TRACE=1: per-phase globaltimer stamps
   // vocab sharding (c4)
   unsigned long long* keys = nullptr;      // [kMaxWindow] packed (value, id) of this pass
@@ -447,6 +448,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.ml_part = h->ml_part;
   P.acnt = h->acnt;
   P.part = h->mega_part;
+  P.epoch = h->mega_epoch;
   P.tile_cnt = h->mega_cnt + 64;
   P.max_tiles = h->mega_max_tiles;
   P.lm_cnt = h->mega_cnt + 1;
@@ -819,13 +821,14 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     int dev_sms = 0;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
     h->sms = dev_sms > 0 ? dev_sms : 148;
-    h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128);
+    h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128 * 2);  // room for u64 tagged partials
+    h->mega_epoch = h->dalloc<unsigned>(1);
     h->mega_max_tiles = (std::max(std::max(h->qd + 2 * h->kvd, 2 * h->I), std::max(h->H, h->v_count)) + 127) / 128;
     h->mega_cnt_words = 64 + size_t(3 + 5 * h->L) * h->mega_max_tiles;
     h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
     h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
-    if (!h->mega_part || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
+    if (!h->mega_part || !h->mega_epoch || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
     if (const char* tr = std::getenv("PS_TRACE"); tr && tr[0] == '1')
       h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 12);
     std::vector<CUtensorMap> wm(size_t(4) * h->L + 1);

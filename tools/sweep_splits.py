@@ -1,4 +1,7 @@
-"""Decode-step time (graph replays) for split-K choices: PS_TC_SPLITS sweeps."""
+"""Decode-step / verify time for values of one environment knob.
+
+    python tools/sweep_splits.py [--var NAME] value...   (default NAME: PS_TC_SPLITS)
+"""
 import os, subprocess, sys, json
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
@@ -22,8 +25,12 @@ for i in range(5):
     v.append(lm.verify_greedy_detail(ctx, cand)["gpu_ms"])
 print("RESULT", statistics.median(ms), statistics.median(v))
 ''' % ROOT
-for combo in sys.argv[1:]:
-    env = dict(os.environ, PS_TC_SPLITS=combo)
+args = sys.argv[1:]
+var = "PS_TC_SPLITS"
+if args[:1] == ["--var"]:
+    var, args = args[1], args[2:]
+for combo in args:
+    env = dict(os.environ, **{var: combo})
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     line = [l for l in out.stdout.splitlines() if l.startswith("RESULT")]
-    print(combo, line[0] if line else out.stderr[-500:], flush=True)
+    print(var, combo, line[0] if line else out.stderr[-500:], flush=True)
