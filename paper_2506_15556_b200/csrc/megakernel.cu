@@ -269,80 +269,228 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
 }
 
 // ---------------------------------------------------------------------------
-constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
-
+// Attention over the paged KV cache (SIMT, fp32 math on bf16 operands).
+//
 // One unit = (kv head, 64-token page s, block of up to kAttnRows query rows).
 // Per (row, q head): scores for the page's keys, page-local softmax stats and
 // P.V; the last page to finish for a (row, kv head) merges all pages in page
-// order. The per-(row, head) arithmetic does not depend on the block/pass.
-__device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, int t0, int t1, int kvh, int s, int n0, float* sm,
-                               int w, int lane, int* rflag, int trace_p = -1) {
-  const bool tr = trace_p >= 0 && threadIdx.x == 64;
-  const int hd = P.hd, grp = P.heads / P.kv_heads;
-  const int kmax = min(kPage, n0 + t1 - 1 + 1 - s * kPage);  // keys needed by the last row of the block
-  float* Ks = sm;                     // [64][hd+1]
-  float* Vs = Ks + kPage * (hd + 1);  // [64][hd], 16-byte aligned rows
-  float* Qs = Vs + kPage * hd;        // [kAttnRows][grp][hd]
-  float* Ps = Qs + kAttnRows * grp * hd;  // [4 warps][4 heads][64] softmax numerators
-  const int tid = threadIdx.x - 64;
-  const size_t page = size_t(P.page_table[s]);
-  const size_t off = size_t(layer) * P.g.layer_stride() + (page * P.kv_heads + kvh) * kPage * hd;
-  // all K/V (and Q) loads of the unit in flight before any is consumed
-  const int vpr = hd / 8;
-  const int nvec = kmax * vpr;  // <= 64 * 16 = 1024 -> <= 8 per thread
-  uint4 kr[8], vr[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = tid + u * kWorkers;
-    if (e < nvec) {
-      const int j = e / vpr, d0 = (e % vpr) * 8;
-      kr[u] = __ldcg(reinterpret_cast<const uint4*>(P.kpool + off + size_t(j) * hd + d0));
-      vr[u] = __ldcg(reinterpret_cast<const uint4*>(P.vpool + off + size_t(j) * hd + d0));
-    }
+// order. The per-(row, head) arithmetic does not depend on the block, the
+// pass width or how heads are spread over warps (batch invariance).
+//
+// Operands are staged raw (bf16) in shared memory with cp.async, two unit
+// buffers: the keys cached by earlier passes are requested while the CTA is
+// still in the layer's QKV phase, only this pass's rows (and q) after the
+// barrier, and unit i+1's loads overlap unit i's math.
+constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
+
+struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf, then Qs, Ps
+  unsigned char* base;
+  int buf, koff_v, koff_q;  // bytes: buffer stride, V and Q offsets within a buffer
+  float* Qs;                // [kAttnRows][grp][hd] fp32 copy of the unit being computed
+  float* Ps;                // [4 warps][4 heads][64] softmax numerators
+  // K: [64][hd + 8] (row pad: conflict-free 16-byte reads by key), V: [64][hd], Q: [kAttnRows][grp][hd]
+  __device__ __forceinline__ __nv_bfloat16* K(int b) const { return reinterpret_cast<__nv_bfloat16*>(base + b * buf); }
+  __device__ __forceinline__ __nv_bfloat16* V(int b) const {
+    return reinterpret_cast<__nv_bfloat16*>(base + b * buf + koff_v);
   }
-  const int nrows = t1 - t0;
-  const int qvec_row = grp * hd / 8;   // uint4 per row of the group's q heads
-  const int nq = nrows * qvec_row;     // <= 4 * 8 * 128 / 8 = 512 -> <= 4 per thread
-  uint4 qr[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int e = tid + u * kWorkers;
-    if (e < nq) {
+  __device__ __forceinline__ __nv_bfloat16* Q(int b) const {
+    return reinterpret_cast<__nv_bfloat16*>(base + b * buf + koff_q);
+  }
+};
+
+__device__ __forceinline__ AttnSmem attn_smem(void* base, int hd, int grp) {
+  AttnSmem a;
+  a.base = static_cast<unsigned char*>(base);
+  a.koff_v = kPage * (hd + 8) * 2;
+  a.koff_q = a.koff_v + kPage * hd * 2;
+  a.buf = a.koff_q + kAttnRows * grp * hd * 2;
+  a.Qs = reinterpret_cast<float*>(a.base + 2 * a.buf);
+  a.Ps = a.Qs + kAttnRows * grp * hd;
+  return a;
+}
+
+__device__ __forceinline__ void cp_async16(const void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct AttnUnit {
+  int t0, t1, kvh, s;
+  bool valid;
+};
+
+// The i-th unit (i >= 0 counts only units with work) of CTA c: units are
+// dealt round-robin (u = c, c + G, ...), page fastest.
+__device__ __forceinline__ AttnUnit attn_unit_from(const MegaParams& P, int rows, int n0, int u_start, int G, int& u_next) {
+  const int npages = (n0 + rows - 1) / kPage + 1;
+  const int nblocks = (rows + kAttnRows - 1) / kAttnRows;
+  const int units = nblocks * P.kv_heads * npages;
+  AttnUnit U{0, 0, 0, 0, false};
+  for (int u = u_start; u < units; u += G) {
+    const int s = u % npages, r = u / npages;
+    const int t0 = (r / P.kv_heads) * kAttnRows, t1 = min(rows, t0 + kAttnRows);
+    if (s > (n0 + t1 - 1) / kPage) continue;  // no row of the block reaches this page
+    U = AttnUnit{t0, t1, r % P.kv_heads, s, true};
+    u_next = u + G;
+    return U;
+  }
+  u_next = units;
+  return U;
+}
+
+// Request a unit's operands into buffer b: part 0 = keys written by earlier
+// passes (positions < n0), part 1 = this pass's keys and the q rows.
+__device__ __forceinline__ void attn_issue(const MegaParams& P, int layer, const AttnUnit& U, int n0, const AttnSmem& A,
+                                           int b, int part, int tid) {
+  const int hd = P.hd, grp = P.heads / P.kv_heads, vpr = hd / 8;
+  const int kmax = min(kPage, n0 + U.t1 - U.s * kPage);  // keys needed by the block's last row
+  const int kc = max(0, min(kmax, n0 - U.s * kPage));    // of which cached before this pass
+  const int jlo = part == 0 ? 0 : kc, jhi = part == 0 ? kc : kmax;
+  const size_t page = size_t(P.page_table[U.s]);
+  const size_t off = size_t(layer) * P.g.layer_stride() + (page * P.kv_heads + U.kvh) * kPage * hd;
+  for (int e = tid; e < (jhi - jlo) * vpr; e += kWorkers) {
+    const int j = jlo + e / vpr, d0 = (e % vpr) * 8;
+    cp_async16(A.K(b) + j * (hd + 8) + d0, P.kpool + off + size_t(j) * hd + d0);
+    cp_async16(A.V(b) + j * hd + d0, P.vpool + off + size_t(j) * hd + d0);
+  }
+  if (part == 1) {
+    const int qvec_row = grp * hd / 8;
+    for (int e = tid; e < (U.t1 - U.t0) * qvec_row; e += kWorkers) {
       const int r = e / qvec_row, rem = (e % qvec_row) * 8;
-      qr[u] = __ldcg(reinterpret_cast<const uint4*>(P.q + size_t(t0 + r) * P.qd + size_t(kvh) * grp * hd + rem));
+      cp_async16(A.Q(b) + e * 8, P.q + size_t(U.t0 + r) * P.qd + size_t(U.kvh) * grp * hd + rem);
     }
   }
+}
+
+// Scores, page-local softmax and P.V for heads [hb, hb + nhh) of query row r
+// (nhh <= NH). Every (row, head) follows the same operation order whatever NH.
+template <int NH>
+__device__ __forceinline__ void attn_heads(const MegaParams& P, const AttnSmem& A, int b, int hd, int grp, int kvh, int s,
+                                           int r, int t, int hb, int nhh, int nkeys, int w, int lane) {
+  const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
+  const __nv_bfloat16* k0 = A.K(b) + (has0 ? lane : 0) * (hd + 8);
+  const __nv_bfloat16* k1 = A.K(b) + (has1 ? lane + 32 : 0) * (hd + 8);
+  const float* qb = A.Qs + (r * grp + hb) * hd;
+  float a0[NH], a1[NH];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = tid + u * kWorkers;
-    if (e < nvec) {
-      const int j = e / vpr, d0 = (e % vpr) * 8;
-      const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kr[u]);
-      const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vr[u]);
+  for (int hh = 0; hh < NH; ++hh) a0[hh] = a1[hh] = 0.f;
+  for (int d = 0; d < hd; d += 8) {
+    const uint4 ka = *reinterpret_cast<const uint4*>(k0 + d);
+    const uint4 kb = *reinterpret_cast<const uint4*>(k1 + d);
+    const __nv_bfloat162* ka2 = reinterpret_cast<const __nv_bfloat162*>(&ka);
+    const __nv_bfloat162* kb2 = reinterpret_cast<const __nv_bfloat162*>(&kb);
+    float kf0[8], kf1[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        Ks[j * (hd + 1) + d0 + i] = __bfloat162float(kb[i]);
-        Vs[j * hd + d0 + i] = __bfloat162float(vb[i]);
+    for (int i = 0; i < 4; ++i) {
+      const float2 x = __bfloat1622float2(ka2[i]), y = __bfloat1622float2(kb2[i]);
+      kf0[2 * i] = x.x;
+      kf0[2 * i + 1] = x.y;
+      kf1[2 * i] = y.x;
+      kf1[2 * i + 1] = y.y;
+    }
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) {
+      if (hh < nhh) {
+#pragma unroll
+        for (int h4 = 0; h4 < 2; ++h4) {
+          const float4 qv = *reinterpret_cast<const float4*>(qb + hh * hd + d + 4 * h4);
+          const float* k0f = kf0 + 4 * h4;
+          const float* k1f = kf1 + 4 * h4;
+          a0[hh] = fmaf(qv.w, k0f[3], fmaf(qv.z, k0f[2], fmaf(qv.y, k0f[1], fmaf(qv.x, k0f[0], a0[hh]))));
+          a1[hh] = fmaf(qv.w, k1f[3], fmaf(qv.z, k1f[2], fmaf(qv.y, k1f[1], fmaf(qv.x, k1f[0], a1[hh]))));
+        }
       }
     }
   }
+  float* Pw = A.Ps + w * 4 * kPage;  // this warp's numerators [4 heads][64 keys]
+  float mxs[NH], ls[NH];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int e = tid + u * kWorkers;
-    if (e < nq) {
-      const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(&qr[u]);
+  for (int hh = 0; hh < NH; ++hh) {
+    mxs[hh] = 0.f;
+    ls[hh] = 0.f;
+    if (hh < nhh) {
+      const float s0 = has0 ? a0[hh] * P.attn_scale : -INFINITY;
+      const float s1 = has1 ? a1[hh] * P.attn_scale : -INFINITY;
+      const float mx = warp_max(fmaxf(s0, s1));
+      const float p0 = has0 ? expf(s0 - mx) : 0.f;
+      const float p1 = has1 ? expf(s1 - mx) : 0.f;
+      ls[hh] = warp_sum(p0 + p1);
+      mxs[hh] = mx;
+      Pw[hh * kPage + lane] = p0;
+      Pw[hh * kPage + lane + 32] = p1;
+    }
+  }
+  __syncwarp();
+  const __nv_bfloat16* Vb = A.V(b);
+  for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+    float4 acc[NH];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) Qs[e * 8 + i] = __bfloat162float(qb[i]);
+    for (int hh = 0; hh < NH; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < nkeys; ++j) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(Vb + j * hd + d4);
+      const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        const float pj = Pw[hh * kPage + j];
+        acc[hh].x = fmaf(pj, v01.x, acc[hh].x);
+        acc[hh].y = fmaf(pj, v01.y, acc[hh].y);
+        acc[hh].z = fmaf(pj, v23.x, acc[hh].z);
+        acc[hh].w = fmaf(pj, v23.y, acc[hh].w);
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) {
+      if (hh < nhh) {
+        const int h = kvh * grp + hb + hh;
+        const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
+        *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc[hh];
+      }
+    }
+  }
+  if (lane < nhh) {
+    const int h = kvh * grp + hb + lane;
+    const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
+    float mxl = mxs[0], ll = ls[0];
+#pragma unroll
+    for (int hh = 1; hh < NH; ++hh)
+      if (lane == hh) {
+        mxl = mxs[hh];
+        ll = ls[hh];
+      }
+    P.ml_part[slot * 2] = mxl;
+    P.ml_part[slot * 2 + 1] = ll;
+  }
+  __syncwarp();
+}
+
+// Math of a unit whose operands are resident in buffer b, then the page
+// arrival count and (for the rows whose last page this was) the page merge.
+__device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUnit& U, int n0, const AttnSmem& A, int b,
+                                               int w, int lane, int* rflag, int trace_p = -1) {
+  const bool tr = trace_p >= 0 && threadIdx.x == 64;
+  const int hd = P.hd, grp = P.heads / P.kv_heads;
+  const int t0 = U.t0, t1 = U.t1, kvh = U.kvh, s = U.s;
+  const int tid = threadIdx.x - 64;
+  const int nrows = t1 - t0;
+  for (int e = tid; e < nrows * grp * hd / 8; e += kWorkers) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(A.Q(b) + e * 8);
+    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(q2[i]);
+      A.Qs[e * 8 + 2 * i] = f.x;
+      A.Qs[e * 8 + 2 * i + 1] = f.y;
     }
   }
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
-  // Work item = (query row, slice of the GQA group's heads), one per warp,
-  // each (row, head) computed identically whatever the slicing: with >= 4 rows
-  // a warp takes a row and all its heads (<= 4 at a time, every K/V element
-  // read from shared memory feeds 4 heads -> 16 FMA chains per lane); with
-  // fewer rows (decode) the heads are spread over the warps. Scores: lane
-  // owns keys lane and lane+32.
+  // Work item = (query row, slice of the GQA group's heads), one per warp:
+  // with >= 4 rows a warp takes a row and all its heads (<= 4 at a time, each
+  // K/V element read from shared memory feeds 4 heads); with fewer rows
+  // (decode) the heads are spread over the warps. Lane owns keys lane, lane+32.
   const int warps_per_row = nrows >= 4 ? 1 : 4 / nrows;
   const int hs = (grp + warps_per_row - 1) / warps_per_row;
   const int nchunk = (grp + hs - 1) / hs;
@@ -351,78 +499,12 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
     const int t = t0 + r, pos = n0 + t;
     if (s > pos / kPage) continue;  // this page is beyond the row's causal range
     const int nkeys = min(kPage, pos + 1 - s * kPage);
-    const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
-    const float* k0 = Ks + (has0 ? lane : 0) * (hd + 1);
-    const float* k1 = Ks + (has1 ? lane + 32 : 0) * (hd + 1);
     for (int hb = h_lo; hb < h_hi; hb += 4) {
       const int nhh = min(4, h_hi - hb);
-      const float* qb = Qs + (r * grp + hb) * hd;
-      float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-      for (int d = 0; d < hd; d += 4) {
-        const float k00 = k0[d], k01 = k0[d + 1], k02 = k0[d + 2], k03 = k0[d + 3];
-        const float k10 = k1[d], k11 = k1[d + 1], k12 = k1[d + 2], k13 = k1[d + 3];
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-          if (hh < nhh) {
-            const float4 qv = *reinterpret_cast<const float4*>(qb + hh * hd + d);
-            a0[hh] = fmaf(qv.w, k03, fmaf(qv.z, k02, fmaf(qv.y, k01, fmaf(qv.x, k00, a0[hh]))));
-            a1[hh] = fmaf(qv.w, k13, fmaf(qv.z, k12, fmaf(qv.y, k11, fmaf(qv.x, k10, a1[hh]))));
-          }
-        }
-      }
-      float* Pw = Ps + w * 4 * kPage;  // this warp's numerators [4 heads][64 keys]
-      float mxs[4], ls[4];
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh) {
-        if (hh < nhh) {
-          const float s0 = has0 ? a0[hh] * P.attn_scale : -INFINITY;
-          const float s1 = has1 ? a1[hh] * P.attn_scale : -INFINITY;
-          const float mx = warp_max(fmaxf(s0, s1));
-          const float p0 = has0 ? expf(s0 - mx) : 0.f;
-          const float p1 = has1 ? expf(s1 - mx) : 0.f;
-          ls[hh] = warp_sum(p0 + p1);
-          mxs[hh] = mx;
-          Pw[hh * kPage + lane] = p0;
-          Pw[hh * kPage + lane + 32] = p1;
-        }
-      }
-      __syncwarp();
-      for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-        float4 acc[4];
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = 0; j < nkeys; ++j) {
-          const float4 vv = *reinterpret_cast<const float4*>(Vs + j * hd + d4);
-#pragma unroll
-          for (int hh = 0; hh < 4; ++hh) {
-            const float pj = Pw[hh * kPage + j];
-            acc[hh].x = fmaf(pj, vv.x, acc[hh].x);
-            acc[hh].y = fmaf(pj, vv.y, acc[hh].y);
-            acc[hh].z = fmaf(pj, vv.z, acc[hh].z);
-            acc[hh].w = fmaf(pj, vv.w, acc[hh].w);
-          }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-          if (hh < nhh) {
-            const int h = kvh * grp + hb + hh;
-            const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-            *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc[hh];
-          }
-        }
-      }
-      if (lane < nhh) {
-        const int h = kvh * grp + hb + lane;
-        const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-        float mxl = mxs[0], ll = ls[0];
-#pragma unroll
-        for (int hh = 1; hh < 4; ++hh)
-          if (lane == hh) { mxl = mxs[hh]; ll = ls[hh]; }
-        P.ml_part[slot * 2] = mxl;
-        P.ml_part[slot * 2 + 1] = ll;
-      }
-      __syncwarp();
+      if (hs == 1)
+        attn_heads<1>(P, A, b, hd, grp, kvh, s, r, t, hb, 1, nkeys, w, lane);
+      else
+        attn_heads<4>(P, A, b, hd, grp, kvh, s, r, t, hb, nhh, nkeys, w, lane);
     }
   }
   wk_bar();
@@ -479,6 +561,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, int layer, i
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
 }
+
 
 // Partial slot of CTA cc's piece of `tile` (slot 0 = the CTA's first tile).
 __device__ __forceinline__ int piece_off(int cc, int tile, const Gemm& g, int m) {
@@ -579,7 +662,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   const int b_bytes = P.ntok * 128;
   auto a_tile = [&](int s) { return base + size_t(s) * (kTileABytes + b_bytes); };
   auto b_tile = [&](int s) { return a_tile(s) + kTileABytes; };
-  float* attn_sm = reinterpret_cast<float*>(base + size_t(ST) * (kTileABytes + b_bytes));
+  const AttnSmem A = attn_smem(base + size_t(ST) * (kTileABytes + b_bytes), P.hd, P.heads / P.kv_heads);
   const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[8]);
   const uint32_t acc_full0 = smem_u32(&bars[16]), acc_empty0 = smem_u32(&bars[18]);
 
@@ -757,6 +840,16 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       }
       wk_bar();
       if (P.ctx->stop) break;
+      if (kind == PH_QKV) {
+        // keys cached by earlier passes for this CTA's first attention unit of
+        // the layer: requested now, consumed after the next barrier
+        int un = 0;
+        const AttnUnit U0 = attn_unit_from(P, rows, n0, c, G, un);
+        if (U0.valid) {
+          attn_issue(P, layer, U0, n0, A, 0, 0, tid);
+          cp_async_commit();
+        }
+      }
       if (kind == PH_FINAL) {
         // argmax of every row over the per-CTA partials of the LM phase;
         // rows are spread over CTAs (t = c, c+G, ...), one warp per row
@@ -788,18 +881,36 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           }
         }
       } else if (kind == PH_ATTN) {
-        const int npages = (n0 + rows - 1) / kPage + 1;
-        const int nblocks = (rows + kAttnRows - 1) / kAttnRows;
-        const int units = nblocks * P.kv_heads * npages;
-        bool first_unit = true;
-        for (int u = c; u < units; u += G) {
-          const int s = u % npages, r = u / npages;
-          const int kvh = r % P.kv_heads, blk = r / P.kv_heads;
-          const int t0 = blk * kAttnRows, t1 = min(rows, t0 + kAttnRows);
-          if (s > (n0 + t1 - 1) / kPage) continue;  // no row of the block reaches this page
-          if (tid == 0 && first_unit) stamp(P, p, c, G, 7);
-          attention_unit(P, layer, t0, t1, kvh, s, n0, attn_sm, w, lane, es.rflag, first_unit ? p : -1);
-          first_unit = false;
+        // double-buffered units; the current unit's cached keys were requested in the QKV phase
+        int un = 0, un2 = 0;
+        AttnUnit cur = attn_unit_from(P, rows, n0, c, G, un);
+        AttnUnit nxt{0, 0, 0, 0, false};
+        if (cur.valid) {
+          attn_issue(P, layer, cur, n0, A, 0, 1, tid);
+          cp_async_commit();
+          nxt = attn_unit_from(P, rows, n0, un, G, un2);
+          if (nxt.valid) {
+            attn_issue(P, layer, nxt, n0, A, 1, 0, tid);
+            attn_issue(P, layer, nxt, n0, A, 1, 1, tid);
+          }
+          cp_async_commit();
+        }
+        for (int i = 0; cur.valid; ++i) {
+          cp_async_wait<1>();  // every group but the newest: the current unit's operands
+          wk_bar();
+          if (tid == 0 && i == 0) stamp(P, p, c, G, 7);
+          attention_unit(P, cur, n0, A, i & 1, w, lane, es.rflag, i == 0 ? p : -1);  // ends with wk_bar
+          AttnUnit nn{0, 0, 0, 0, false};
+          int un3 = un2;
+          if (nxt.valid) nn = attn_unit_from(P, rows, n0, un2, G, un3);
+          if (nn.valid) {  // into the buffer just consumed
+            attn_issue(P, layer, nn, n0, A, i & 1, 0, tid);
+            attn_issue(P, layer, nn, n0, A, i & 1, 1, tid);
+          }
+          cp_async_commit();
+          cur = nxt;
+          nxt = nn;
+          un2 = un3;
         }
       } else {
         if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {

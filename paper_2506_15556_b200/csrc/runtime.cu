@@ -406,7 +406,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   using bf = __nv_bfloat16;
   const int ntok = round_up(std::max(max_rows, 1), 16);
   const int grp = h->nh / h->nkv;
-  const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + 4 * grp * h->hd + 16 * kPage;
+  const int attn_floats = mega_attn_bytes(h->hd, grp) / 4;
   MegaParams P{};
   P.ctx = ctx;
   P.decode = decode ? 1 : 0;
@@ -852,7 +852,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     cudaMemcpy(h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
     // every pass width must fit one CTA per SM (co-residency of the grid)
     const int grp = h->nh / h->nkv;
-    const int attn_floats = kPage * (h->hd + 1) + kPage * h->hd + 4 * grp * h->hd + 16 * kPage;
+    const int attn_floats = mega_attn_bytes(h->hd, grp) / 4;
     for (int ntok = 16; ntok <= kMaxWindow; ntok += 16) {
       const int st = mega_stages(ntok, attn_floats);
       if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats)) < 1)
