@@ -209,11 +209,8 @@ struct MegaParams {
   unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
 };
 // attention staging of the megakernel (see AttnSmem in megakernel.cu): two
-// unit buffers of bf16 K [64][hd+8], V [64][hd], q [4][grp][hd], plus fp32 q
-// and softmax numerators
-inline int mega_attn_bytes(int hd, int grp) {
-  return 2 * (kPage * (hd + 8) * 2 + kPage * hd * 2 + 4 * grp * hd * 2) + 4 * grp * hd * 4 + 16 * kPage * 4;
-}
+// unit buffers of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
+inline int mega_attn_bytes(int hd, int grp) { return 2 * (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2); }
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);
 cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st);

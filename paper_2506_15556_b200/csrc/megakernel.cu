@@ -283,12 +283,12 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
 // barrier, and unit i+1's loads overlap unit i's math.
 constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
 
-struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf, then Qs, Ps
+struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf
   unsigned char* base;
   int buf, koff_v, koff_q;  // bytes: buffer stride, V and Q offsets within a buffer
-  float* Qs;                // [kAttnRows][grp][hd] fp32 copy of the unit being computed
-  float* Ps;                // [4 warps][4 heads][64] softmax numerators
-  // K: [64][hd + 8] (row pad: conflict-free 16-byte reads by key), V: [64][hd], Q: [kAttnRows][grp][hd]
+  // rows padded to hd + 8 elements (272 B for hd = 128): the 8 rows touched by
+  // one fragment load / ldmatrix phase fall in distinct banks
+  // K: [64 keys][hd + 8], V: [64 keys][hd + 8], Q: [kAttnRows * grp pairs][hd + 8]
   __device__ __forceinline__ __nv_bfloat16* K(int b) const { return reinterpret_cast<__nv_bfloat16*>(base + b * buf); }
   __device__ __forceinline__ __nv_bfloat16* V(int b) const {
     return reinterpret_cast<__nv_bfloat16*>(base + b * buf + koff_v);
@@ -302,10 +302,8 @@ __device__ __forceinline__ AttnSmem attn_smem(void* base, int hd, int grp) {
   AttnSmem a;
   a.base = static_cast<unsigned char*>(base);
   a.koff_v = kPage * (hd + 8) * 2;
-  a.koff_q = a.koff_v + kPage * hd * 2;
-  a.buf = a.koff_q + kAttnRows * grp * hd * 2;
-  a.Qs = reinterpret_cast<float*>(a.base + 2 * a.buf);
-  a.Ps = a.Qs + kAttnRows * grp * hd;
+  a.koff_q = 2 * a.koff_v;
+  a.buf = a.koff_q + kAttnRows * grp * (hd + 8) * 2;
   return a;
 }
 
@@ -353,121 +351,47 @@ __device__ __forceinline__ void attn_issue(const MegaParams& P, int layer, const
   for (int e = tid; e < (jhi - jlo) * vpr; e += kWorkers) {
     const int j = jlo + e / vpr, d0 = (e % vpr) * 8;
     cp_async16(A.K(b) + j * (hd + 8) + d0, P.kpool + off + size_t(j) * hd + d0);
-    cp_async16(A.V(b) + j * hd + d0, P.vpool + off + size_t(j) * hd + d0);
+    cp_async16(A.V(b) + j * (hd + 8) + d0, P.vpool + off + size_t(j) * hd + d0);
   }
   if (part == 1) {
+    // V rows past the last needed key meet p = 0 in the tensor-core P.V: they
+    // must be finite, so zero them (stale shared memory may hold NaN bits)
+    for (int e = tid; e < (kPage - kmax) * vpr; e += kWorkers) {
+      const int j = kmax + e / vpr, d0 = (e % vpr) * 8;
+      *reinterpret_cast<uint4*>(A.V(b) + j * (hd + 8) + d0) = make_uint4(0u, 0u, 0u, 0u);
+    }
     const int qvec_row = grp * hd / 8;
     for (int e = tid; e < (U.t1 - U.t0) * qvec_row; e += kWorkers) {
       const int r = e / qvec_row, rem = (e % qvec_row) * 8;
-      cp_async16(A.Q(b) + e * 8, P.q + size_t(U.t0 + r) * P.qd + size_t(U.kvh) * grp * hd + rem);
+      // pair (r, head) -> Q row r * grp + head
+      cp_async16(A.Q(b) + (r * grp + rem / hd) * (hd + 8) + rem % hd,
+                 P.q + size_t(U.t0 + r) * P.qd + size_t(U.kvh) * grp * hd + rem);
     }
   }
 }
 
-// Scores, page-local softmax and P.V for heads [hb, hb + nhh) of query row r
-// (nhh <= NH). Every (row, head) follows the same operation order whatever NH.
-template <int NH>
-__device__ __forceinline__ void attn_heads(const MegaParams& P, const AttnSmem& A, int b, int hd, int grp, int kvh, int s,
-                                           int r, int t, int hb, int nhh, int nkeys, int w, int lane) {
-  const bool has0 = lane < nkeys, has1 = lane + 32 < nkeys;
-  const __nv_bfloat16* k0 = A.K(b) + (has0 ? lane : 0) * (hd + 8);
-  const __nv_bfloat16* k1 = A.K(b) + (has1 ? lane + 32 : 0) * (hd + 8);
-  const float* qb = A.Qs + (r * grp + hb) * hd;
-  float a0[NH], a1[NH];
-#pragma unroll
-  for (int hh = 0; hh < NH; ++hh) a0[hh] = a1[hh] = 0.f;
-  for (int d = 0; d < hd; d += 8) {
-    const uint4 ka = *reinterpret_cast<const uint4*>(k0 + d);
-    const uint4 kb = *reinterpret_cast<const uint4*>(k1 + d);
-    const __nv_bfloat162* ka2 = reinterpret_cast<const __nv_bfloat162*>(&ka);
-    const __nv_bfloat162* kb2 = reinterpret_cast<const __nv_bfloat162*>(&kb);
-    float kf0[8], kf1[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 x = __bfloat1622float2(ka2[i]), y = __bfloat1622float2(kb2[i]);
-      kf0[2 * i] = x.x;
-      kf0[2 * i + 1] = x.y;
-      kf1[2 * i] = y.x;
-      kf1[2 * i + 1] = y.y;
-    }
-#pragma unroll
-    for (int hh = 0; hh < NH; ++hh) {
-      if (hh < nhh) {
-#pragma unroll
-        for (int h4 = 0; h4 < 2; ++h4) {
-          const float4 qv = *reinterpret_cast<const float4*>(qb + hh * hd + d + 4 * h4);
-          const float* k0f = kf0 + 4 * h4;
-          const float* k1f = kf1 + 4 * h4;
-          a0[hh] = fmaf(qv.w, k0f[3], fmaf(qv.z, k0f[2], fmaf(qv.y, k0f[1], fmaf(qv.x, k0f[0], a0[hh]))));
-          a1[hh] = fmaf(qv.w, k1f[3], fmaf(qv.z, k1f[2], fmaf(qv.y, k1f[1], fmaf(qv.x, k1f[0], a1[hh]))));
-        }
-      }
-    }
-  }
-  float* Pw = A.Ps + w * 4 * kPage;  // this warp's numerators [4 heads][64 keys]
-  float mxs[NH], ls[NH];
-#pragma unroll
-  for (int hh = 0; hh < NH; ++hh) {
-    mxs[hh] = 0.f;
-    ls[hh] = 0.f;
-    if (hh < nhh) {
-      const float s0 = has0 ? a0[hh] * P.attn_scale : -INFINITY;
-      const float s1 = has1 ? a1[hh] * P.attn_scale : -INFINITY;
-      const float mx = warp_max(fmaxf(s0, s1));
-      const float p0 = has0 ? expf(s0 - mx) : 0.f;
-      const float p1 = has1 ? expf(s1 - mx) : 0.f;
-      ls[hh] = warp_sum(p0 + p1);
-      mxs[hh] = mx;
-      Pw[hh * kPage + lane] = p0;
-      Pw[hh * kPage + lane + 32] = p1;
-    }
-  }
-  __syncwarp();
-  const __nv_bfloat16* Vb = A.V(b);
-  for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-    float4 acc[NH];
-#pragma unroll
-    for (int hh = 0; hh < NH; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < nkeys; ++j) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(Vb + j * hd + d4);
-      const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-      const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh) {
-        const float pj = Pw[hh * kPage + j];
-        acc[hh].x = fmaf(pj, v01.x, acc[hh].x);
-        acc[hh].y = fmaf(pj, v01.y, acc[hh].y);
-        acc[hh].z = fmaf(pj, v23.x, acc[hh].z);
-        acc[hh].w = fmaf(pj, v23.y, acc[hh].w);
-      }
-    }
-#pragma unroll
-    for (int hh = 0; hh < NH; ++hh) {
-      if (hh < nhh) {
-        const int h = kvh * grp + hb + hh;
-        const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-        *reinterpret_cast<float4*>(P.o_part + slot * hd + d4) = acc[hh];
-      }
-    }
-  }
-  if (lane < nhh) {
-    const int h = kvh * grp + hb + lane;
-    const size_t slot = (size_t(t) * P.heads + h) * P.max_splits_attn + s;
-    float mxl = mxs[0], ll = ls[0];
-#pragma unroll
-    for (int hh = 1; hh < NH; ++hh)
-      if (lane == hh) {
-        mxl = mxs[hh];
-        ll = ls[hh];
-      }
-    P.ml_part[slot * 2] = mxl;
-    P.ml_part[slot * 2 + 1] = ll;
-  }
-  __syncwarp();
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Math of a unit whose operands are resident in buffer b, then the page
-// arrival count and (for the rows whose last page this was) the page merge.
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Math of a unit whose operands are resident in buffer b, on the tensor cores
+// (mma.sync m16n8k16, bf16 in / fp32 accumulate): M = the unit's (row, head)
+// pairs in tiles of 16, N = keys (S) or head dims (O), K = head dims (S) or
+// keys (O). Every warp computes S for the whole page (64 keys) and the
+// page-local softmax in registers, then P.V for its quarter of the head dims;
+// P enters the second product as a bf16 hi + lo pair (~16-bit mantissa). An
+// output row depends only on its own (row, head) pair, never on where the
+// pair sits in the tile, so 1-row decode and wide verify agree bitwise.
+// Then the page arrival count and, for rows whose last page this was, the merge.
 __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUnit& U, int n0, const AttnSmem& A, int b,
                                                int w, int lane, int* rflag, int trace_p = -1) {
   const bool tr = trace_p >= 0 && threadIdx.x == 64;
@@ -475,36 +399,115 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
   const int t0 = U.t0, t1 = U.t1, kvh = U.kvh, s = U.s;
   const int tid = threadIdx.x - 64;
   const int nrows = t1 - t0;
-  for (int e = tid; e < nrows * grp * hd / 8; e += kWorkers) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(A.Q(b) + e * 8);
-    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __bfloat1622float2(q2[i]);
-      A.Qs[e * 8 + 2 * i] = f.x;
-      A.Qs[e * 8 + 2 * i + 1] = f.y;
-    }
-  }
-  wk_bar();
+  const int npairs = nrows * grp;
+  const int ld = (hd + 8) / 2;  // row stride in 32-bit words
+  const uint32_t* Q32 = reinterpret_cast<const uint32_t*>(A.Q(b));
+  const uint32_t* K32 = reinterpret_cast<const uint32_t*>(A.K(b));
+  const uint32_t vbase = smem_u32(A.V(b));
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
-  // Work item = (query row, slice of the GQA group's heads), one per warp:
-  // with >= 4 rows a warp takes a row and all its heads (<= 4 at a time, each
-  // K/V element read from shared memory feeds 4 heads); with fewer rows
-  // (decode) the heads are spread over the warps. Lane owns keys lane, lane+32.
-  const int warps_per_row = nrows >= 4 ? 1 : 4 / nrows;
-  const int hs = (grp + warps_per_row - 1) / warps_per_row;
-  const int nchunk = (grp + hs - 1) / hs;
-  for (int item = w; item < nrows * nchunk; item += 4) {
-    const int r = item / nchunk, h_lo = (item % nchunk) * hs, h_hi = min(grp, h_lo + hs);
-    const int t = t0 + r, pos = n0 + t;
-    if (s > pos / kPage) continue;  // this page is beyond the row's causal range
-    const int nkeys = min(kPage, pos + 1 - s * kPage);
-    for (int hb = h_lo; hb < h_hi; hb += 4) {
-      const int nhh = min(4, h_hi - hb);
-      if (hs == 1)
-        attn_heads<1>(P, A, b, hd, grp, kvh, s, r, t, hb, 1, nkeys, w, lane);
-      else
-        attn_heads<4>(P, A, b, hd, grp, kvh, s, r, t, hb, nhh, nkeys, w, lane);
+  const int g8 = lane >> 2, q4 = lane & 3;
+  for (int mt = 0; mt * 16 < npairs; ++mt) {
+    const int p0 = mt * 16 + g8, p1 = p0 + 8;
+    const bool in0 = p0 < npairs, in1 = p1 < npairs;
+    // ---- S = Q K^T for 16 pairs x 64 keys
+    float S[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) S[nt][0] = S[nt][1] = S[nt][2] = S[nt][3] = 0.f;
+    for (int ks = 0; ks < hd / 16; ++ks) {
+      const int kw = ks * 8 + q4;  // word column of this lane's first two dims
+      const uint32_t a0 = in0 ? Q32[p0 * ld + kw] : 0u, a1 = in1 ? Q32[p1 * ld + kw] : 0u;
+      const uint32_t a2 = in0 ? Q32[p0 * ld + kw + 4] : 0u, a3 = in1 ? Q32[p1 * ld + kw + 4] : 0u;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const uint32_t* kr = K32 + (nt * 8 + g8) * ld + kw;
+        mma_bf16(S[nt], a0, a1, a2, a3, kr[0], kr[4]);
+      }
+    }
+    // ---- causal mask + page-local softmax; rows p0 (S[.][0..1]) and p1 (S[.][2..3])
+    int nk[2];
+    float mx[2], l[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int pp = h ? p1 : p0;
+      const int pos = n0 + t0 + pp / grp;
+      nk[h] = (pp < npairs) ? min(kPage, pos + 1 - s * kPage) : 0;  // <= 0: the row does not reach this page
+      float m = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = nt * 8 + q4 * 2 + e;
+          const float v = key < nk[h] ? S[nt][2 * h + e] * P.attn_scale : -INFINITY;
+          S[nt][2 * h + e] = v;
+          m = fmaxf(m, v);
+        }
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      if (nk[h] <= 0) m = 0.f;
+      float sum = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float pv = nk[h] > 0 ? expf(S[nt][2 * h + e] - m) : 0.f;  // exp(-inf) = 0 past the mask
+          S[nt][2 * h + e] = pv;
+          sum += pv;
+        }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      mx[h] = m;
+      l[h] = sum;
+    }
+    // ---- O = P V for this warp's quarter of the head dims (n-tiles of 8)
+    const int ndt = hd / 32;  // dim tiles per warp
+    float O[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {  // 16 keys per step: S n-tiles 2kk, 2kk+1
+      uint32_t ah[4], al[4];
+      const float* x0 = S[2 * kk];
+      const float* x1 = S[2 * kk + 1];
+      const float src[4][2] = {{x0[0], x0[1]}, {x0[2], x0[3]}, {x1[0], x1[1]}, {x1[2], x1[3]}};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(src[i][0], src[i][1]);
+        const float2 hf = __bfloat1622float2(hi);
+        ah[i] = *reinterpret_cast<const uint32_t*>(&hi);
+        al[i] = pack_bf16(src[i][0] - hf.x, src[i][1] - hf.y);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < ndt) {
+          const int dt = w * ndt + i;
+          // V[keys kk*16 .. +16][dims dt*8 .. +8], transposed into the B fragment
+          const uint32_t addr = vbase + uint32_t(((kk * 16 + (lane & 15)) * (hd + 8) + dt * 8) * 2);
+          uint32_t b0, b1;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                       : "=r"(b0), "=r"(b1)
+                       : "r"(addr));
+          mma_bf16(O[i], ah[0], ah[1], ah[2], ah[3], b0, b1);
+          mma_bf16(O[i], al[0], al[1], al[2], al[3], b0, b1);
+        }
+      }
+    }
+    // ---- page-local outputs of the pairs whose row reaches this page
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (nk[h] <= 0) continue;
+      const int pp = h ? p1 : p0;
+      const int t = t0 + pp / grp, head = kvh * grp + pp % grp;
+      const size_t slot = (size_t(t) * P.heads + head) * P.max_splits_attn + s;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < ndt) {
+          const int dim = (w * ndt + i) * 8 + q4 * 2;
+          *reinterpret_cast<float2*>(P.o_part + slot * hd + dim) = make_float2(O[i][2 * h], O[i][2 * h + 1]);
+        }
+      if (w == 0 && q4 == 0) {
+        P.ml_part[slot * 2] = mx[h];
+        P.ml_part[slot * 2 + 1] = l[h];
+      }
     }
   }
   wk_bar();
@@ -524,38 +527,48 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
   }
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
-  for (int r = 0; r < nrows; ++r) {
+  // merge, one warp per (row, head): lane sp owns page sp for the scalars
+  // (fixed butterfly); the output sums run over pages in order, loads batched
+  for (int it = w; it < nrows * grp; it += 4) {
+    const int r = it / grp, hh = it % grp;
     if (!rflag[r]) continue;
     const int t = t0 + r, pos = n0 + t;
     const int nsplit = pos / kPage + 1;
-    // merge: lane sp owns page sp for the scalars (fixed butterfly); the
-    // output sums run over pages in order
-    for (int hh = w; hh < grp; hh += 4) {
-      const int h = kvh * grp + hh;
-      const size_t base = (size_t(t) * P.heads + h) * P.max_splits_attn;
-      float M = -INFINITY;
-      for (int sp = lane; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
-      M = warp_max(M);
-      float Lp = 0.f;
-      for (int sp = lane; sp < nsplit; sp += 32)
-        Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
-      const float L = warp_sum(Lp);
-      for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int sp = 0; sp < nsplit; ++sp) {
-          const float f = expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
-          const float4 o = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp) * hd + d4));
-          acc.x = fmaf(o.x, f, acc.x);
-          acc.y = fmaf(o.y, f, acc.y);
-          acc.z = fmaf(o.z, f, acc.z);
-          acc.w = fmaf(o.w, f, acc.w);
-        }
-        __nv_bfloat16* dst = P.attn + size_t(t) * P.qd + size_t(h) * hd + d4;
-        dst[0] = __float2bfloat16_rn(acc.x / L);
-        dst[1] = __float2bfloat16_rn(acc.y / L);
-        dst[2] = __float2bfloat16_rn(acc.z / L);
-        dst[3] = __float2bfloat16_rn(acc.w / L);
+    const int h = kvh * grp + hh;
+    const size_t base = (size_t(t) * P.heads + h) * P.max_splits_attn;
+    float M = -INFINITY;
+    for (int sp = lane; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
+    M = warp_max(M);
+    float Lp = 0.f;
+    for (int sp = lane; sp < nsplit; sp += 32)
+      Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
+    const float L = warp_sum(Lp);
+    for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sp0 = 0; sp0 < nsplit; sp0 += 8) {
+        float mv[8];
+        float4 o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (sp0 + u < nsplit) {
+            mv[u] = __ldcg(P.ml_part + (base + sp0 + u) * 2);
+            o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp0 + u) * hd + d4));
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (sp0 + u < nsplit) {
+            const float f = expf(mv[u] - M);
+            acc.x = fmaf(o[u].x, f, acc.x);
+            acc.y = fmaf(o[u].y, f, acc.y);
+            acc.z = fmaf(o[u].z, f, acc.z);
+            acc.w = fmaf(o[u].w, f, acc.w);
+          }
       }
+      __nv_bfloat16* dst = P.attn + size_t(t) * P.qd + size_t(h) * hd + d4;
+      dst[0] = __float2bfloat16_rn(acc.x / L);
+      dst[1] = __float2bfloat16_rn(acc.y / L);
+      dst[2] = __float2bfloat16_rn(acc.z / L);
+      dst[3] = __float2bfloat16_rn(acc.w / L);
     }
   }
   wk_bar();

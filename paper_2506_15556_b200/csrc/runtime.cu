@@ -817,6 +817,9 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       !h->h_argmax || !h->h_steps_tok)
     return bad("workspace");
   h->mega = h->bf16;
+  // the megakernel's attention fragments: head_dim a multiple of 32, at most 128
+  if (h->mega && (h->hd % 32 != 0 || h->hd > 128))
+    return (ps_destroy(h), fail(PS_ERR_UNSUPPORTED, "bf16 path needs head_dim in {32, 64, 96, 128}"));
   if (h->mega) {
     int dev_sms = 0;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
