@@ -96,6 +96,19 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
                      int32_t n_cand, int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out,
                      float* gpu_ms);
 
+/* Fused top-k verify: the greedy pass, then the rank of every candidate token
+ * in its row, rank = #{j : s_j > s_t or (s_j == s_t and j < t)} over the fp32
+ * logits the pass's LM head produced (no sort, no host rows); k = the longest
+ * prefix of cand whose ranks are < topk. KV rolled back to len(prompt)+k.
+ * rank_out (nullable) gets the n_cand ranks; the other outputs are as in
+ * ps_verify_greedy. topk == 1 accepts exactly what ps_verify_greedy accepts.
+ * Unsupported (PS_ERR_UNSUPPORTED) on a vocab-sharded LM head.
+ * Replaces `verify_topk` -> `_verify_by_rule` with `topk_tokens`
+ * (verify.py:100-113, lm.py:139-145). */
+int ps_verify_topk(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand,
+                   int32_t n_cand, int32_t topk, int32_t* k_out, int32_t* first_term_out,
+                   int32_t* argmax_out, int32_t* rank_out, float* gpu_ms);
+
 /* Greedy continuation of seq[0..n_seq): up to max_tokens argmax tokens, the
  * first from row n_seq-1 (free when already resident), the rest from
  * back-to-back 1-row decode steps replayed from a CUDA graph without host

@@ -113,7 +113,7 @@ class DecoderOracle:
 
     def _operand(self, x):
         """(GEMM operand, output scale): fp32 mode normalises first; bf16 mode
-        feeds bf16(x) and scales the product by rstd (csrc/gemm_tc.cu)."""
+        feeds bf16(x) and scales the product by rstd (the GEMM epilogues of csrc/megakernel.cu)."""
         if self.bf16:
             rstd = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + self.eps)
             return self._r(x), rstd

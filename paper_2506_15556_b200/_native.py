@@ -73,6 +73,8 @@ SIGNATURES = {
     "ps_logits_rows": (ctypes.c_int, [_h, ctypes.c_int32, ctypes.c_int32, _f32p]),
     "ps_verify_greedy": (ctypes.c_int, [_h, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p, _i32p, _i32p,
                                         _f32p]),
+    "ps_verify_topk": (ctypes.c_int, [_h, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, ctypes.c_int32, _i32p,
+                                      _i32p, _i32p, _i32p, _f32p]),
     "ps_decode_greedy": (ctypes.c_int, [_h, _i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p,
                                         _f32p]),
     "ps_truncate": (ctypes.c_int, [_h, ctypes.c_int32]),

@@ -248,6 +248,28 @@ class B200LM(LanguageModel):
                    am, ctypes.byref(ms))
         return {"k": k.value, "first_term": term.value, "argmax": list(am), "gpu_ms": ms.value}
 
+    def verify_topk_fused(self, prompt, candidate, topk: int):
+        """Fused top-k verify (rank counting on the device): (k, handle over prompt ++ candidate, cost)."""
+        if not prompt:
+            raise ValueError("verification requires a nonempty prompt context")
+        d = self.verify_topk_detail(prompt, candidate, topk)
+        self.last_verify_ms = d["gpu_ms"]
+        self.verify_ms.append(d["gpu_ms"])
+        seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)
+        return d["k"], CacheHandle(seq, self._backend_id), self._cost(len(seq), d["gpu_ms"])
+
+    def verify_topk_detail(self, prompt, candidate, topk: int) -> dict:
+        """Fused top-k verify returning every device output, ranks included."""
+        p = _native.i32_array(prompt)
+        c = _native.i32_array(candidate)
+        k, term, ms = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_float()
+        am = (ctypes.c_int32 * (len(candidate) + 1))()
+        rk = (ctypes.c_int32 * max(1, len(candidate)))()
+        self._call("ps_verify_topk", p, len(prompt), c, len(candidate), int(topk), ctypes.byref(k),
+                   ctypes.byref(term), am, rk, ctypes.byref(ms))
+        return {"k": k.value, "first_term": term.value, "argmax": list(am), "rank": list(rk)[: len(candidate)],
+                "gpu_ms": ms.value}
+
     def decode_greedy_fused(self, seq, n: int):
         """Up to n greedy tokens continuing `seq` (stops after EOS): [(token, cost_ms)]."""
         if n <= 0:

@@ -23,7 +23,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libpredgen_b200.so"
 OBJ = PKG / "_build"
-SOURCES = ["init.cu", "layers.cu", "gemm_simt.cu", "gemm_tc.cu", "megakernel.cu", "runtime.cu"]
+SOURCES = ["init.cu", "layers.cu", "gemm_simt.cu", "tma.cu", "megakernel.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

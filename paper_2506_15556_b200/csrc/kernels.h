@@ -95,6 +95,8 @@ void launch_argmax_reduce(const PassCtx* ctx, int max_rows, const float* am_val,
 
 // Greedy verify epilogue: k = first i with argmax_pos[p0-1+i] != cand[i];
 // first terminator index in cand; writes {k, first_term} to res.
+// rank of each candidate token in its row's logits (ties -> lower id first)
+void launch_topk_rank(const float* logits, int ld, int V, const int* cand, int n, int* rank, cudaStream_t st);
 void launch_verify_compare(const int* argmax_pos, int p0, const int* cand, int n_cand,
                            const unsigned char* term_mask, int* res, cudaStream_t st);
 
@@ -104,65 +106,14 @@ void launch_shard_unpack(PassCtx* ctx, const unsigned long long* keys, unsigned 
 // decode-step bookkeeping: advance n0 unless stopped.
 void launch_advance(PassCtx* ctx, cudaStream_t st);
 
-// ---- bf16 tcgen05 path (gemm_tc.cu) ----
+// ---- bf16 tensor maps (tma.cu) ----
 struct TmaDesc {
   alignas(64) unsigned char bytes[128];
 };
 bool encode_tma_2d_bf16(TmaDesc* out, const void* base, uint64_t inner, uint64_t outer,
                         uint32_t box_inner, uint32_t box_outer);
-// Fused epilogues of the tcgen05 weight-streaming GEMM. Split-K partials
-// are summed (in split order) by the last-arriving CTA of each 128-row tile,
-// which then applies the epilogue for its rows:
-//   QKV    * rstd + bias, RoPE, q -> q buffer, k/v -> paged KV
-//   SWIGLU * rstd, act = silu(gate) * up   (gate/up rows interleaved per tile)
-//   RESID  x += y; xb = bf16(x); per-tile sum of squares -> the grid's last
-//          tile writes rstd per row (the next GEMM applies it: y = rstd*W.xb)
-//   ARGMAX logits = rstd * (E.xb) + bias; per-tile (max, lowest id); the
-//          grid's last tile reduces over tiles -> argmax_pos[n0+t]
-enum TcMode : int { TC_EPI_QKV = 0, TC_EPI_SWIGLU = 1, TC_EPI_RESID = 2, TC_EPI_ARGMAX = 3 };
-struct TcEpilogue {
-  int mode = 0;
-  float* part = nullptr;             // split-K partials [split][kMaxWindow][N]
-  unsigned* tile_cnt = nullptr;      // per-tile arrival counters (self-resetting)
-  unsigned* grid_cnt = nullptr;      // grid-wide arrival counter (RESID / ARGMAX)
-  const float* rstd_in = nullptr;    // per-row rstd (QKV/SWIGLU: [t]; ARGMAX: [n0+t])
-  // QKV
-  const __nv_bfloat16* bias = nullptr;
-  const float2* rope = nullptr;
-  __nv_bfloat16* q = nullptr;
-  __nv_bfloat16* kpool = nullptr;
-  __nv_bfloat16* vpool = nullptr;
-  const int* page_table = nullptr;
-  KvGeom g{};
-  int layer = 0, q_dim = 0, kv_dim = 0;
-  // SWIGLU
-  __nv_bfloat16* act = nullptr;
-  int inter = 0;
-  // RESID
-  float* x = nullptr;
-  __nv_bfloat16* xb_out = nullptr;
-  int xb_out_pos = 0;                // 1: row index n0+t (hn_cache) instead of t
-  float* ssq_part = nullptr;         // [tile][kMaxWindow]
-  float* rstd_out = nullptr;
-  int rstd_out_pos = 0;
-  int hidden = 0;
-  float eps = 0.f;
-  // ARGMAX
-  const float* lbias = nullptr;
-  int v_begin = 0;
-  float* am_val = nullptr;
-  int* am_idx = nullptr;
-  float* logits_out = nullptr;
-  int ld_logits = 0;
-  int* argmax_pos = nullptr;
-  unsigned long long* packed_out = nullptr;
-  int advance = 0;                   // decode step: last CTA advances ctx->n0
-};
-void launch_tc(PassCtx* ctx, const TmaDesc* tmW, const TmaDesc* tmX, int N, int K, int splits, int ntok,
-               int x_row_from_ctx, const TcEpilogue& e, cudaStream_t st, bool pdl);
 
 constexpr int kTileTc = 128;
-int tc_gemm_smem_bytes(int ntok);
 
 // ---- persistent megakernel (megakernel.cu): one cooperative launch per pass ----
 struct MegaParams {
@@ -206,6 +157,9 @@ struct MegaParams {
   int* am_idx;
   unsigned long long* keys;
   unsigned* bar;            // grid barrier counter, zeroed before launch
+  int lm_only;              // 1: LM head + argmax over resident rows [n0, n0+rows) only (hn / rstd caches)
+  float* logits_out;        // optional fp32 logits [rows][ld_logits] from the LM epilogue
+  int ld_logits;
   unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
 };
 // attention staging of the megakernel (see AttnSmem in megakernel.cu): two

@@ -376,6 +376,40 @@ void launch_verify_compare(const int* argmax_pos, int p0, const int* cand, int n
   verify_compare_kernel<<<1, 32, 0, st>>>(argmax_pos, p0, cand, n_cand, term_mask, res);
 }
 
+// Top-k verification rule (verify_topk, verify.py:100-113; topk_tokens,
+// lm.py:139-145): candidate token t of row i is inside the top k iff its rank
+// #{j : s_j > s_t  or  (s_j == s_t and j < t)} is below k. No sort: every
+// block counts a slice of the vocabulary for one row and adds its integer
+// count (order-free, so exact). logits: [n][ld] fp32, the LM phase's values.
+__global__ void topk_rank_kernel(const float* __restrict__ logits, int ld, int V, const int* __restrict__ cand, int n,
+                                 int* __restrict__ rank) {
+  const int i = blockIdx.y;
+  if (i >= n) return;
+  const int t = cand[i];
+  const float* row = logits + size_t(i) * ld;
+  const float st = row[t];
+  int cnt = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < V; j += gridDim.x * blockDim.x) {
+    const float sj = row[j];
+    cnt += (sj > st || (sj == st && j < t)) ? 1 : 0;
+  }
+  cnt = warp_sum_int(cnt);
+  __shared__ int part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) tot += part[w];
+    if (tot) atomicAdd(rank + i, tot);
+  }
+}
+
+void launch_topk_rank(const float* logits, int ld, int V, const int* cand, int n, int* rank, cudaStream_t st) {
+  cudaMemsetAsync(rank, 0, sizeof(int) * n, st);
+  const dim3 grid((V + 256 * 16 - 1) / (256 * 16), n);
+  topk_rank_kernel<<<grid, 256, 0, st>>>(logits, ld, V, cand, n, rank);
+}
+
 // Vocab-sharded LM head: after the packed (value, id) keys of this pass were
 // MAX-all-reduced across shards (or not, when merge == 0), store them per
 // position and decode the global argmax; in decode mode also advance n0.

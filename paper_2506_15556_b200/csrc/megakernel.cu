@@ -236,6 +236,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       if (valid && t < rows) {
         lv = v[j] * es.rstd[t] + b;
         li = vid;
+        if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n] = lv;  // exactly the values the argmax sees
       }
       warp_argmax(lv, li);
       if (lane == 0 && t < rows) argmax_merge(es.am_v[q][t], es.am_i[q][t], lv, li);
@@ -703,6 +704,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   const int n0 = P.ctx->n0;
   const int rows = P.ctx->rows;
   const int nphases = 3 + 5 * P.L;
+  // LM-only passes (logits of resident rows) start at the LM phase; barrier
+  // generation g counts the phases completed so far (the embed is generation 1)
+  const int p_first = P.lm_only ? 1 + 5 * P.L : 1;
 
   if (warp == 0) {
     // ======================= TMA producer =======================
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         const int xrow_lm = n0;
         const uint64_t pol_stream = l2_policy_evict_first();
         uint32_t it = 0;
-        for (int p = 1; p < nphases; ++p) {
+        for (int p = p_first; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
           if (kind == PH_ATTN || kind == PH_FINAL) continue;
           const Gemm g = gemm_of(P, kind);
@@ -737,7 +741,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
             tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
           }
-          grid_wait(P.bar, unsigned(G) * unsigned(p));  // activations of this phase are complete
+          grid_wait(P.bar, unsigned(G) * unsigned(p - p_first + 1));  // activations of this phase are complete
           stamp(P, p, c, G, 0);
           fence_proxy_async_global();
           for (int i = 0; i < pre; ++i) {
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       if (!P.ctx->stop) {
         const uint32_t idesc = idesc_bf16(P.ntok);
         uint32_t it = 0, acc_it = 0;
-        for (int p = 1; p < nphases; ++p) {
+        for (int p = p_first; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
           if (kind == PH_ATTN || kind == PH_FINAL) continue;
           const Gemm g = gemm_of(P, kind);
@@ -803,7 +807,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
     const int tid = threadIdx.x - 64;
     uint32_t acc_it = 0;
     // ---- phase 0: embedding rows (t ≡ c mod G) ----
-    for (int t = c; t < rows; t += G) {
+    for (int t = c; t < (P.lm_only ? 0 : rows); t += G) {
       const int pos = n0 + t;
       if (tid == 0) {
         int tok;
@@ -844,11 +848,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       stamp(P, 0, c, G, 2);
       grid_arrive(P.bar);
     }
-    for (int p = 1; p < nphases; ++p) {
+    for (int p = p_first; p < nphases; ++p) {
       const int kind = phase_kind(p, P.L);
       const int layer = kind == PH_LM ? P.L - 1 : (p - 1) / 5;
       if (tid == 0) {
-        grid_wait(P.bar, unsigned(G) * unsigned(p));
+        grid_wait(P.bar, unsigned(G) * unsigned(p - p_first + 1));
         stamp(P, p, c, G, 1);
       }
       wk_bar();
@@ -926,7 +930,10 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           un2 = un3;
         }
       } else {
-        if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {
+        if (P.lm_only) {  // LM head over resident rows: the final rstd of each position is cached
+          for (int t = tid; t < rows; t += kWorkers) es.rstd[t] = P.rstd_cache[n0 + t];
+          wk_bar();
+        } else if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {
           load_rstd(P, kind == PH_QKV && layer == 0, rows, w, lane, es);
           wk_bar();
           if (kind == PH_LM && c == 0)

@@ -219,7 +219,7 @@ struct ps_handle {
 
   PassCtx* h_ctx = nullptr;   // pinned ring [kCtxSlots]
   int* h_tok = nullptr;       // pinned ring [kCtxSlots][kMaxWindow]
-  int* h_res = nullptr;       // pinned [4]
+  int* h_res = nullptr;       // pinned [4 + kMaxWindow]
   int* h_argmax = nullptr;    // pinned [max_seq + kMaxWindow]
   int* h_steps_tok = nullptr; // pinned [kMaxSteps]
   int ring = 0;
@@ -401,8 +401,11 @@ void enqueue_shard_merge(ps_handle* h, PassCtx* ctx, int max_rows, bool decode) 
   launch_shard_unpack(ctx, h->keys, h->keys_pos, h->argmax_pos, h->nccl_comm ? 1 : 0, decode ? 1 : 0, h->st);
 }
 
-// bf16 pass as ONE persistent cooperative kernel (megakernel.cu).
-void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, bool decode) {
+// bf16 pass as ONE persistent cooperative kernel (megakernel.cu). lm_only:
+// LM head + argmax over resident rows [ctx->n0, +rows) from the per-position
+// hn / rstd caches (logits_out, if given, receives the fp32 logits).
+void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, bool decode, bool lm_only = false,
+                  float* logits_out = nullptr) {
   using bf = __nv_bfloat16;
   const int ntok = round_up(std::max(max_rows, 1), 16);
   const int grp = h->nh / h->nkv;
@@ -454,14 +457,17 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.lm_cnt = h->mega_cnt + 1;
   P.am_val = h->am_val;
   P.am_idx = h->am_idx;
-  P.keys = sharded ? h->keys : nullptr;
+  P.keys = (sharded && !lm_only) ? h->keys : nullptr;
   P.bar = h->mega_cnt;
+  P.lm_only = lm_only ? 1 : 0;
+  P.logits_out = logits_out;
+  P.ld_logits = h->v_count;
   P.trace = h->mega_trace;
   cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned) * h->mega_cnt_words, h->st);
   prof_mark(h, 7);
   const cudaError_t e = launch_mega(P, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
   if (e != cudaSuccess) std::fprintf(stderr, "predgen_b200: megakernel launch failed: %s\n", cudaGetErrorString(e));
-  if (sharded) enqueue_shard_merge(h, ctx, max_rows, decode);
+  if (sharded && !lm_only) enqueue_shard_merge(h, ctx, max_rows, decode);
   prof_mark(h, 6);
 }
 
@@ -794,7 +800,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->rope = h->dalloc<float2>(seq_rows * (h->hd / 2));
   h->d_tok = h->dalloc<int>(kMaxWindow);
   h->d_cand = h->dalloc<int>(c.max_seq);
-  h->d_res = h->dalloc<int>(4);
+  h->d_res = h->dalloc<int>(4 + kMaxWindow);  // [k, first_term, -, -, top-k ranks...]
   h->rstd = h->dalloc<float>(kMaxWindow);
   h->rstd_cache = h->dalloc<float>(seq_rows);
   h->ssq_part = h->dalloc<float>(size_t(4) * (H / kTileTc + 1) * kMaxWindow);
@@ -808,7 +814,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   h->d_ctx_aux = h->dalloc<PassCtx>(1);
   h->h_ctx = h->halloc<PassCtx>(kCtxSlots);
   h->h_tok = h->halloc<int>(size_t(kCtxSlots) * kMaxWindow);
-  h->h_res = h->halloc<int>(4);
+  h->h_res = h->halloc<int>(4 + kMaxWindow);
   h->h_argmax = h->halloc<int>(seq_rows);
   h->h_steps_tok = h->halloc<int>(std::max(kMaxSteps, c.max_seq));
   if (!h->x || !h->xn || !h->q || !h->attn || !h->act || !h->part || !h->o_part || !h->ml_part || !h->hn_cache ||
@@ -921,50 +927,42 @@ int ps_forward(ps_handle* h, const int32_t* tokens, int32_t n, int32_t row_from,
   return PS_OK;
 }
 
-int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
-  if (!h || !out || first < 0 || n <= 0 || first + n > int(h->resident.size()))
-    return fail(PS_ERR_INVALID, "logits rows outside the resident sequence");
-  CK(cudaSetDevice(h->cfg.device));
+namespace {
+
+// fp32 logits of resident rows [first, first + rows) into h->logits_buf, by the
+// same LM-head arithmetic the passes used (bf16: the megakernel's LM phase in
+// LM-only mode; fp32: lmhead_f32_kernel), so every value is the one the device
+// argmax saw. rows <= kMaxWindow. Enqueued on h->st.
+int enqueue_logits_rows(ps_handle* h, int first, int rows) {
   if (!h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
-  for (int done = 0; done < n;) {
-    const int rows = std::min(kMaxWindow, n - done);
-    int slot;
-    PassCtx* hc = next_ctx_slot(h, &slot);
-    *hc = PassCtx{first + done, rows, 0, 0, 0, {0, 0, 0}};
-    CK(copy_async(h, h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
-    if (h->bf16) {
-      const ActDescs* ad = act_descs(h, round_up(rows, 16));
-      if (!ad) return fail(PS_ERR_CUDA, "TMA descriptor encode failed");
-      TcEpilogue a;
-      a.mode = TC_EPI_ARGMAX;
-      a.grid_cnt = h->counters + 4096 + 3;
-      a.rstd_in = h->rstd_cache;
-      a.lbias = h->lm_bias;
-      a.v_begin = h->v_begin;
-      a.am_val = h->am_val;
-      a.am_idx = h->am_idx;
-      a.argmax_pos = h->argmax_pos;  // rewrites the same ids it already holds
-      a.logits_out = h->logits_buf;
-      a.ld_logits = h->v_count;
-      launch_tc(h->d_ctx_aux, &h->tm_head, &ad->hn, h->v_count, h->H, 1, round_up(rows, 16), 1, a, h->st, false);
-    } else {
-      launch_lmhead_f32(h->d_ctx_aux, rows, static_cast<const float*>(h->hn_cache), 0,
-                        static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
-                        h->am_idx, h->logits_buf, h->v_count, h->st);
-    }
-    CK(copy_async(h, out + size_t(done) * h->v_count, h->logits_buf, sizeof(float) * size_t(rows) * h->v_count,
-                  cudaMemcpyDeviceToHost));
-    CK(cudaStreamSynchronize(h->st));
-    done += rows;
+  int slot;
+  PassCtx* hc = next_ctx_slot(h, &slot);
+  *hc = PassCtx{first, rows, 0, 0, 0, {0, 0, 0}};
+  CK(copy_async(h, h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
+  if (h->bf16) {
+    enqueue_mega(h, h->d_ctx_aux, rows, nullptr, false, true, h->logits_buf);
+  } else {
+    launch_lmhead_f32(h->d_ctx_aux, rows, static_cast<const float*>(h->hn_cache), 0,
+                      static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
+                      h->am_idx, h->logits_buf, h->v_count, h->st);
   }
-  CK(cudaGetLastError());
+  h->stats.launches += 1;
   return PS_OK;
 }
 
-int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand, int32_t n_cand,
-                     int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out, float* gpu_ms) {
+// Shared by ps_verify_greedy (topk == 0) and ps_verify_topk: one pass over the
+// non-resident tail of P ++ R, the compare / first-terminator kernel, and for
+// top-k the rank of every candidate token in its row; KV rolled back to |P| + k.
+int verify_impl(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand, int32_t n_cand,
+                int32_t topk, int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out, int32_t* rank_out,
+                float* gpu_ms) {
   if (!h || !prompt || n_prompt <= 0 || n_cand < 0 || (n_cand > 0 && !cand))
     return fail(PS_ERR_INVALID, "verification requires a nonempty prompt context");
+  if (topk > 0 && n_cand > kMaxWindow) return fail(PS_ERR_INVALID, "top-k verification: candidate longer than 256");
+  if (topk > 0 && h->cfg.vocab_shards > 1)
+    return fail(PS_ERR_UNSUPPORTED, "top-k verification over a vocab-sharded LM head is not implemented");
+  for (int i = 0; i < n_cand; ++i)
+    if (cand[i] < 0 || cand[i] >= h->cfg.vocab) return fail(PS_ERR_INVALID, "candidate token id out of range");
   CK(cudaSetDevice(h->cfg.device));
   std::vector<int> seq(prompt, prompt + n_prompt);
   if (n_cand) seq.insert(seq.end(), cand, cand + n_cand);
@@ -986,7 +984,12 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
     CK(copy_async(h, h->d_cand, src, sizeof(int) * n_cand, cudaMemcpyHostToDevice));
     launch_verify_compare(h->argmax_pos, n_prompt, h->d_cand, n_cand, h->term_mask, h->d_res, h->st);
     h->stats.launches += 1;
-    CK(copy_async(h, h->h_res, h->d_res, sizeof(int) * 2, cudaMemcpyDeviceToHost));
+    if (topk > 0) {  // rows n_prompt-1 .. n_prompt+n_cand-2 score the candidate tokens
+      if (int rc = enqueue_logits_rows(h, n_prompt - 1, n_cand)) return rc;
+      launch_topk_rank(h->logits_buf, h->v_count, h->v_count, h->d_cand, n_cand, h->d_res + 4, h->st);
+      h->stats.launches += 1;
+    }
+    CK(copy_async(h, h->h_res, h->d_res, sizeof(int) * (topk > 0 ? 4 + n_cand : 2), cudaMemcpyDeviceToHost));
   }
   CK(cudaEventRecord(h->ev1, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -995,7 +998,16 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev0, h->ev1);
   h->stats.gpu_ms += ms;
-  const int k = n_cand ? h->h_res[0] : 0;
+  int k = n_cand ? h->h_res[0] : 0;
+  if (topk > 0) {  // maximal prefix whose tokens rank inside the top k
+    k = n_cand;
+    for (int i = 0; i < n_cand; ++i)
+      if (h->h_res[4 + i] >= topk) {
+        k = i;
+        break;
+      }
+    if (rank_out) std::memcpy(rank_out, h->h_res + 4, sizeof(int) * n_cand);
+  }
   const int first_term = n_cand ? h->h_res[1] : -1;
   if (argmax_out) std::memcpy(argmax_out, h->argmax_host.data() + (n_prompt - 1), sizeof(int) * (n_cand + 1));
   truncate_to(h, n_prompt + k);  // KV rollback to the accepted prefix
@@ -1003,6 +1015,36 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
   if (first_term_out) *first_term_out = first_term;
   if (gpu_ms) *gpu_ms = ms;
   return PS_OK;
+}
+
+}  // namespace
+
+int ps_logits_rows(ps_handle* h, int32_t first, int32_t n, float* out) {
+  if (!h || !out || first < 0 || n <= 0 || first + n > int(h->resident.size()))
+    return fail(PS_ERR_INVALID, "logits rows outside the resident sequence");
+  CK(cudaSetDevice(h->cfg.device));
+  for (int done = 0; done < n;) {
+    const int rows = std::min(kMaxWindow, n - done);
+    if (int rc = enqueue_logits_rows(h, first + done, rows)) return rc;
+    CK(copy_async(h, out + size_t(done) * h->v_count, h->logits_buf, sizeof(float) * size_t(rows) * h->v_count,
+                  cudaMemcpyDeviceToHost));
+    CK(cudaStreamSynchronize(h->st));
+    done += rows;
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand, int32_t n_cand,
+                     int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out, float* gpu_ms) {
+  return verify_impl(h, prompt, n_prompt, cand, n_cand, 0, k_out, first_term_out, argmax_out, nullptr, gpu_ms);
+}
+
+int ps_verify_topk(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int32_t* cand, int32_t n_cand,
+                   int32_t topk, int32_t* k_out, int32_t* first_term_out, int32_t* argmax_out, int32_t* rank_out,
+                   float* gpu_ms) {
+  if (topk < 1) return fail(PS_ERR_INVALID, "top-k verification requires k >= 1");
+  return verify_impl(h, prompt, n_prompt, cand, n_cand, topk, k_out, first_term_out, argmax_out, rank_out, gpu_ms);
 }
 
 int ps_decode_greedy(ps_handle* h, const int32_t* seq, int32_t n_seq, int32_t max_tokens, int32_t stop_at_eos,

@@ -1,5 +1,5 @@
 // tcgen05 / TMA / mbarrier building blocks shared by the weight-streaming
-// GEMM kernels (gemm_tc.cu) and the persistent decode kernel (megakernel.cu).
+// persistent decode / verify kernel (megakernel.cu).
 #pragma once
 
 #include <cuda.h>

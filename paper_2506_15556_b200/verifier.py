@@ -10,10 +10,12 @@ API and accounting of the reference's `specstream.verify`
   R[:k]; nfe 1; uncached = len(P)+len(R) (`verify.py:63-97`).
 * `verify_topk`, `verify_reflection`, `make_verifier` (`verify.py:100-175`).
 
-B200 fast path: when the backend exposes `verify_greedy_fused(P, R)` (the
+B200 fast paths: when the backend exposes `verify_greedy_fused(P, R)` (the
 `ps_verify_greedy` C-ABI call), the pass, the per-row argmax, the compare and
-the first-mismatch scan all run on the device and only k comes back; the
-outcome is field-for-field what the generic path computes.
+the first-mismatch scan all run on the device and only k comes back; with
+`verify_topk_fused(P, R, k)` (`ps_verify_topk`) the candidate ranks are
+counted on the device from the pass's own logits. Either outcome is
+field-for-field what the generic path computes.
 """
 
 from __future__ import annotations
@@ -88,8 +90,15 @@ def verify_greedy(prompt, candidate, lm, clock=None) -> VerifierOutcome:
 def verify_topk(prompt, candidate, lm, k: int, clock=None) -> VerifierOutcome:
     if k < 1:
         raise ValueError("top-k verification requires k >= 1")
-    return _verify_with_rule(prompt, candidate, lm,
-                             lambda row, tok: tok in topk_tokens(row, k), clock)
+    fused = getattr(lm, "verify_topk_fused", None)
+    if fused is None or getattr(lm, "vocab_shards", 1) > 1:
+        return _verify_with_rule(prompt, candidate, lm,
+                                 lambda row, tok: tok in topk_tokens(row, k), clock)
+    if not prompt:
+        raise ValueError("verification requires a nonempty prompt context")
+    acc, handle, cost = fused(list(prompt), list(candidate), k)
+    _charge(clock, cost)
+    return _outcome(prompt, candidate, acc, handle, cost, lm.vocab)
 
 
 def verify_reflection(prompt, candidate, lm, clock=None, judge_prompt_text=None) -> VerifierOutcome:
