@@ -269,5 +269,13 @@ class CpuDecoderLM:
         return LogitsBlock(rows, start), CacheHandle(ctx, self._backend_id), self.latency.pass_cost(len(ctx) - start)
 
     def judge_consistency(self, partial_prompt, partial_answer):
-        from .lm_surface import JudgeUnsupportedError
-        raise JudgeUnsupportedError("CpuDecoderLM has no consistency judge")
+        """PredGen self-judgment (verify.py:116-158 calls it): one fresh pass over
+        the formatted judge prompt (lm.py:117-131), then the last row's scores of
+        "yes" and "no" (lm.py:107-114). Judge text is mapped to ids by the
+        vocabulary's `judge_ids` (host tokenisation, identical on both sides)."""
+        from .lm_surface import JUDGE_TEMPLATE, JudgeResult
+        ids = self.vocab.judge_ids
+        toks = ids(JUDGE_TEMPLATE.format(partial_prompt=partial_prompt, partial_answer=partial_answer))
+        block, _, cost = self.forward(toks)
+        row = block.last_row
+        return JudgeResult(yes_score=float(row[ids("yes")[0]]), no_score=float(row[ids("no")[0]])), cost

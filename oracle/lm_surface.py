@@ -71,5 +71,28 @@ class LogitsBlock:
 _ids = itertools.count(1_000_000)
 
 
+@dataclass(frozen=True)
+class JudgeResult:
+    """lm.py:107-114: consistent iff yes_score > no_score."""
+    yes_score: float
+    no_score: float
+
+    @property
+    def consistent(self) -> bool:
+        return self.yes_score > self.no_score
+
+
+# lm.py:117-126, verbatim template text (a data constant of the reference API)
+JUDGE_TEMPLATE = (
+    "<|im_start|>user\n"
+    "You are given an incomplete prompt and the model's speculative partial answer.\n"
+    "Please judge whether the partial prompt is consistent with the model's answer.\n"
+    "Partial Prompt: {partial_prompt}\n"
+    "Partial Answer: {partial_answer}\n"
+    "<|im_end|>\n"
+    "<|im_start|>assistant\n"
+)
+
+
 def fresh_backend_id() -> int:
     return next(_ids)

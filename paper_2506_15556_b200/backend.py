@@ -33,7 +33,8 @@ import math
 import numpy as np
 
 from . import _native
-from .model_api import CacheHandle, LanguageModel, LatencyModel, LogitsBlock, PrefixViolationError
+from .model_api import (CacheHandle, JudgeUnsupportedError, LanguageModel, LatencyModel, LogitsBlock,
+                        PrefixViolationError, decoder_judge)
 from .shapes import MODE_BF16, DecoderShape
 from .vocab import SyntheticVocabulary, terminator_mask
 
@@ -220,6 +221,13 @@ class B200LM(LanguageModel):
         argmax, _, ms = self._sync(list(ctx), start)
         rows = _LazyRows(self, ctx, start, argmax)
         return LogitsBlock(rows, start), CacheHandle(ctx, self._backend_id), self._cost(len(ctx) - start, ms)
+
+    def judge_consistency(self, partial_prompt: str, partial_answer: str):
+        """Self-consistency judge (verify_reflection, verify.py:116-158): a pass over the
+        judge prompt on the device, yes/no scores from the exact fp32 last row."""
+        if self.vocab_shards > 1:
+            raise JudgeUnsupportedError("the judge needs the full LM-head row (vocab-sharded instance)")
+        return decoder_judge(self, partial_prompt, partial_answer)
 
     # -- fused fast paths (used by this package's verifier / generator) ------------------
     def verify_greedy_fused(self, prompt, candidate):

@@ -110,6 +110,19 @@ CONSISTENCY_JUDGE_TEMPLATE = (
 )
 
 
+def decoder_judge(lm, partial_prompt: str, partial_answer: str):
+    """PredGen's self-consistency judge for a decoder backend: one fresh
+    forward pass over the formatted judge prompt (lm.py:117-131), then the
+    last row's scores of the words "yes" and "no" (`JudgeResult.consistent`
+    iff yes > no, lm.py:107-114). Returns (JudgeResult, cost of the pass)."""
+    ids = lm.vocab.judge_ids
+    toks = ids(format_judge_prompt(partial_prompt, partial_answer))
+    block, _, cost = lm.forward(toks)
+    row = block.last_row
+    yes, no = ids("yes")[0], ids("no")[0]
+    return JudgeResult(yes_score=float(row[yes]), no_score=float(row[no])), cost
+
+
 def format_judge_prompt(partial_prompt: str, partial_answer: str) -> str:
     return CONSISTENCY_JUDGE_TEMPLATE.format(partial_prompt=partial_prompt,
                                              partial_answer=partial_answer)

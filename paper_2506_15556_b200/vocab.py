@@ -162,6 +162,23 @@ class SyntheticVocabulary:
     def word_ids(self) -> range:
         return range(len(self._SPECIAL), self._size)
 
+    def judge_ids(self, text: str) -> list[int]:
+        """Token ids for judge text (the consistency-judge template is English,
+        which the synthetic table cannot spell): known surfaces keep their ids,
+        any other word maps to a word id by 64-bit FNV-1a of its UTF-8 bytes.
+        One id per `split_words` word, so a pass over it costs what
+        `judge_cost` charges (lm.py:208-213)."""
+        out = []
+        for w in split_words(text):
+            try:
+                out.append(self.id_of(w))
+            except VocabularyError:
+                h = 0xCBF29CE484222325
+                for b in w.encode("utf-8"):
+                    h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+                out.append(len(self._SPECIAL) + h % (self._size - len(self._SPECIAL)))
+        return out
+
 
 @dataclass(frozen=True)
 class SentenceSpan:

@@ -75,3 +75,30 @@ def test_tiny_turn_replay_matches_reference(i):
         assert res.final_text == rec[arm]["final_text"]
         assert [e.to_dict() for e in res.events] == rec[arm]["events"]
     assert rec["speculative"]["final_text"] == rec["baseline"]["final_text"]  # lossless
+
+
+def test_judge_tokens_and_reflection_on_the_oracle():
+    """Self-judgment (verify_reflection, verify.py:116-158) on the decoder oracle:
+    judge text maps to one id per split word (so a pass costs `judge_cost`),
+    known surfaces keep their ids, unknown words hash into the word ids, and the
+    verdict is yes > no on the last row of the judge pass."""
+    from paper_2506_15556_b200.model_api import format_judge_prompt
+    from paper_2506_15556_b200.verifier import verify_reflection
+    from paper_2506_15556_b200.vocab import split_words
+
+    vocab = SyntheticVocabulary(TINY.vocab)
+    ids = vocab.judge_ids("Partial Prompt: w12 w13 . yes")
+    assert ids[3:6] == [12, 13, 1] and all(4 <= i < TINY.vocab for i in ids[:3] + ids[6:])
+    assert ids == vocab.judge_ids("Partial Prompt: w12 w13 . yes")  # deterministic
+    lm = CpuDecoderLM(TINY.as_dict(), vocab, seed=0, latency=LatencyModel())
+    verdict, cost = lm.judge_consistency("w10 w11 w12", "w40 w41 .")
+    text = format_judge_prompt("w10 w11 w12", "w40 w41 .")
+    assert cost == lm.latency.pass_cost(len(split_words(text)))
+    block, _, _ = lm.forward(vocab.judge_ids(text))
+    row = block.last_row
+    assert verdict.yes_score == float(row[vocab.judge_ids("yes")[0]])
+    assert verdict.consistent == (verdict.yes_score > verdict.no_score)
+    out = verify_reflection([5, 6, 7, 8], [40, 41, 1, 50], lm)
+    assert out.judge_fallback in (None, "judge_rejected")
+    if out.judge_fallback is None:
+        assert out.accepted_count == 3 and out.first_sentence_accepted
