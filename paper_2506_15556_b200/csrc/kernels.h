@@ -122,6 +122,7 @@ struct MegaParams {
   int advance;              // decode: last LM CTA advances ctx->n0
   const int* tok_in;        // extend passes
   int L, H, qd, kvd, I, hd, heads, kv_heads, vocab_local, v_begin;
+  int hd_shift;             // log2(hd): hd is 64 or 128 on the bf16 path
   int ntok, stages, acc_cols, max_splits_attn;
   float eps, attn_scale;
   const CUtensorMap* wmaps; // [4L + 1] device-resident tensor maps
@@ -161,13 +162,16 @@ struct MegaParams {
   float* logits_out;        // optional fp32 logits [rows][ld_logits] from the LM epilogue
   int ld_logits;
   unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
+  int pre_max;              // weight stages issued ahead of a phase barrier (<= stages)
+  int pf[8];                // per phase kind: weight boxes L2-prefetched ahead of the phase barrier
 };
 // attention staging of the megakernel (see AttnSmem in megakernel.cu): two
 // unit buffers of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
 inline int mega_attn_bytes(int hd, int grp) { return 2 * (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2); }
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);
-cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st);
+// wide: the pass may have more than one row (max_rows > 1)
+cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cudaStream_t st);
 int mega_max_blocks_per_sm(int smem);
 
 }  // namespace ps

@@ -112,7 +112,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // barrier, 2 workers finished the phase, 3 MMA issue finished, 4 workers saw
 // the last accumulator, 5 workers published all partials, 6 workers done with
 // the deferred finalisation
-constexpr int kTraceSlots = 12;
+constexpr int kTraceSlots = 16;
 __device__ __forceinline__ void stamp(const MegaParams& P, int p, int c, int G, int slot) {
   if (P.trace) P.trace[(size_t(p) * G + c) * kTraceSlots + slot] = gtime();
 }
@@ -152,25 +152,53 @@ struct EpiSmem {
 // (sum of squares, argmax) stay per warp quadrant and are combined by their
 // consumer in a fixed order.
 // NR: rows the call site can have in this chunk (8, or 1 for the decode finaliser).
+// Per-row inputs of a chunk's finishing math that do not depend on the
+// accumulator (RoPE cos/sin and KV page for QKV, the residual for O/D): the
+// call sites issue them together with the partial loads / ahead of the TMEM
+// read, so a chunk costs one memory round trip.
+struct EpiPre {
+  float a[8], b[8];
+  int c[8];
+};
+
+template <int NR = 8>
+__device__ __forceinline__ void epi_load(const MegaParams& P, int kind, int rows, int n0, int tile, int m, int c0,
+                                         EpiPre& e) {
+  const int n = tile * 128 + m;
+  if (kind == PH_QKV) {
+    const int half = P.hd >> 1, pi = (n & (P.hd - 1)) >> 1;
+    const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int t = c0 + j, pos = n0 + t;
+      const float2 cs = (t < rows && (is_q || is_k)) ? __ldg(P.rope + size_t(pos) * half + pi) : make_float2(1.f, 0.f);
+      e.a[j] = cs.x;
+      e.b[j] = cs.y;
+      e.c[j] = (t < rows && !is_q) ? __ldg(P.page_table + pos / kPage) : 0;
+    }
+  } else if (kind == PH_O || kind == PH_D) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) e.a[j] = (c0 + j < rows) ? __ldcg(P.x + size_t(c0 + j) * P.H + n) : 0.f;
+  }
+}
+
 template <int NR = 8>
 __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows, int n0, int tile, int m, int q,
-                             int lane, int c0, const float (&v)[8], EpiSmem& es, const float* xo_pre = nullptr) {
+                             int lane, int c0, const float (&v)[8], EpiSmem& es, const EpiPre& pre) {
   const int n = tile * 128 + m;
   if (kind == PH_QKV) {
     const int hd = P.hd, half = hd >> 1;
-    const int r = n % hd, pi = r >> 1;
+    const int r = n & (hd - 1), pi = r >> 1;  // hd is 64 or 128 (ps_create)
     const bool even = (r & 1) == 0;
     const int dim = even ? pi : pi + half;  // dimension within the head
     const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
     const float bias = P.qkv_bias ? __bfloat162float(P.qkv_bias[size_t(layer) * (P.qd + 2 * P.kvd) + n]) : 0.f;
-    // every global load of the chunk first (no aliasing with the stores below)
     float2 cs[NR];
     int page[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const int t = c0 + j, pos = n0 + t;
-      cs[j] = (t < rows && (is_q || is_k)) ? __ldg(P.rope + size_t(pos) * half + pi) : make_float2(1.f, 0.f);
-      page[j] = (t < rows && !is_q) ? __ldg(P.page_table + pos / kPage) : 0;
+      cs[j] = make_float2(pre.a[j], pre.b[j]);
+      page[j] = pre.c[j];
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
@@ -188,9 +216,9 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
         P.q[size_t(t) * P.qd + col] = ob;
       } else {
         const int cc = col - P.qd - (is_k ? 0 : P.kvd);
-        const int h = cc / hd;
+        const int h = cc >> P.hd_shift;
         const size_t off = size_t(layer) * P.g.layer_stride() +
-                           ((size_t(page[j]) * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc % hd);
+                           ((size_t(page[j]) * P.g.kv_heads + h) * kPage + pos % kPage) * hd + (cc & (hd - 1));
         (is_k ? P.kpool : P.vpool)[off] = ob;
       }
     }
@@ -205,66 +233,135 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
-    float xo[NR];
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-      xo[j] = xo_pre ? xo_pre[j] : (c0 + j < rows) ? __ldcg(P.x + size_t(c0 + j) * P.H + n) : 0.f;
+    const float* xo = pre.a;
+    float sq[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
-      float sq = 0.f;
+      sq[j] = 0.f;
       if (t < rows) {
         float* xp = P.x + size_t(t) * P.H + n;
         const float xi = xo[j] + v[j];
         *xp = xi;
         __nv_bfloat16* dst = to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H;
         dst[n] = __float2bfloat16_rn(xi);
-        sq = xi * xi;
+        sq[j] = xi * xi;
       }
-      sq = warp_sum(sq);
-      if (lane == 0 && t < rows) P.ssq_part[size_t(tile * 4 + q) * kMaxWindow + t] = sq;
+    }
+    if constexpr (NR == 8) {
+      // transposed butterfly over the 8 rows: lane l pairs with l^16, l^8, l^4,
+      // l^2, l^1 exactly as warp_sum does (and a + b == b + a), so each row's
+      // sum is bitwise the decode step's; lane 4r ends with row r
+#pragma unroll
+      for (int step = 0; step < 3; ++step) {
+        const int half = 4 >> step;
+        const bool hi = (lane >> (4 - step)) & 1;
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+          const float send = hi ? sq[k] : sq[half + k];
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 16 >> step);
+          if (hi) sq[k] = sq[half + k];
+          sq[k] += recv;
+        }
+      }
+      sq[0] += __shfl_xor_sync(0xffffffffu, sq[0], 2);
+      sq[0] += __shfl_xor_sync(0xffffffffu, sq[0], 1);
+      const int t = c0 + (lane >> 2);
+      if ((lane & 3) == 0 && t < rows) P.ssq_part[size_t(tile * 4 + q) * kMaxWindow + t] = sq[0];
+    } else {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const int t = c0 + j;
+        const float r = warp_sum(sq[j]);
+        if (lane == 0 && t < rows) P.ssq_part[size_t(tile * 4 + q) * kMaxWindow + t] = r;
+      }
     }
   } else {  // PH_LM: logits = rstd * acc + bias; per-quadrant (max, lowest id)
     const bool valid = n < P.vocab_local;
     const int vid = P.v_begin + n;
     const float b = valid ? P.lm_bias[vid] : 0.f;
+    float lv[NR];
+    int li[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
-      float lv = -INFINITY;
-      int li = 0x7fffffff;
+      lv[j] = -INFINITY;
+      li[j] = 0x7fffffff;
       if (valid && t < rows) {
-        lv = v[j] * es.rstd[t] + b;
-        li = vid;
-        if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n] = lv;  // exactly the values the argmax sees
+        lv[j] = v[j] * es.rstd[t] + b;
+        li[j] = vid;
+        if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n] = lv[j];  // exactly the values the argmax sees
       }
-      warp_argmax(lv, li);
-      if (lane == 0 && t < rows) argmax_merge(es.am_v[q][t], es.am_i[q][t], lv, li);
+    }
+    if constexpr (NR == 8) {
+      // transposed butterfly: each step halves the rows a lane carries (xor 16,
+      // 8, 4), then xor 2, 1 finish; lane 4r ends with row r. (max, lowest id)
+      // is a total order, so the tree does not change the result.
+#pragma unroll
+      for (int step = 0; step < 3; ++step) {
+        const int half = 4 >> step;  // rows kept after this step
+        const bool hi = (lane >> (4 - step)) & 1;
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+          const float sv = hi ? lv[k] : lv[half + k];
+          const int si = hi ? li[k] : li[half + k];
+          const float rv = __shfl_xor_sync(0xffffffffu, sv, 16 >> step);
+          const int ri = __shfl_xor_sync(0xffffffffu, si, 16 >> step);
+          if (hi) { lv[k] = lv[half + k]; li[k] = li[half + k]; }
+          argmax_merge(lv[k], li[k], rv, ri);
+        }
+      }
+#pragma unroll
+      for (int o = 2; o > 0; o >>= 1) {
+        const float rv = __shfl_xor_sync(0xffffffffu, lv[0], o);
+        const int ri = __shfl_xor_sync(0xffffffffu, li[0], o);
+        argmax_merge(lv[0], li[0], rv, ri);
+      }
+      const int t = c0 + (lane >> 2);
+      if ((lane & 3) == 0 && t < rows) argmax_merge(es.am_v[q][t], es.am_i[q][t], lv[0], li[0]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const int t = c0 + j;
+        warp_argmax(lv[j], li[j]);
+        if (lane == 0 && t < rows) argmax_merge(es.am_v[q][t], es.am_i[q][t], lv[j], li[j]);
+      }
     }
   }
 }
 
 // rstd of every row of the pass from the per-tile sums of squares of the
 // previous RESID phase (or the embed rstd), one warp per row, fixed tree.
+// Rows are processed kRstdBatch at a time with every load in flight (a wide
+// pass has up to 256 rows; one L2 round trip per row was the verify pass's
+// largest worker cost).
+constexpr int kRstdBatch = 4;
 __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, EpiSmem& es) {
-  const int ntiles = P.H / 128;
-  for (int t = w; t < rows; t += 4) {
-    if (from_embed) {
-      if (lane == 0) es.rstd[t] = __ldcg(P.rstd0 + t);
-    } else {
-      // 4 quadrant partials per tile; lane sums entries lane, lane+32, ... in order
-      const int nparts = 4 * ntiles;  // <= 4 * 64
-      float vals[8];
+  if (from_embed) {
+    for (int t = w * 32 + lane; t < rows; t += kWorkers) es.rstd[t] = __ldcg(P.rstd0 + t);
+    return;
+  }
+  // 4 quadrant partials per tile; lane sums entries lane, lane+32, ... in order
+  const int nparts = 4 * (P.H / 128);  // <= 4 * 64
+  for (int t0 = w; t0 < rows; t0 += 4 * kRstdBatch) {
+    float vals[kRstdBatch][8];
+#pragma unroll
+    for (int r = 0; r < kRstdBatch; ++r) {
+      const int t = t0 + 4 * r;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = lane + 32 * u;
-        vals[u] = e < nparts ? __ldcg(P.ssq_part + size_t(e) * kMaxWindow + t) : 0.f;
+        vals[r][u] = (t < rows && e < nparts) ? __ldcg(P.ssq_part + size_t(e) * kMaxWindow + t) : 0.f;
       }
+    }
+#pragma unroll
+    for (int r = 0; r < kRstdBatch; ++r) {
+      const int t = t0 + 4 * r;
       float a = 0.f;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a += vals[u];
+      for (int u = 0; u < 8; ++u) a += vals[r][u];
       const float ssq = warp_sum(a);
-      if (lane == 0) es.rstd[t] = 1.0f / sqrtf(ssq / float(P.H) + P.eps);
+      if (lane == 0 && t < rows) es.rstd[t] = 1.0f / sqrtf(ssq / float(P.H) + P.eps);
     }
   }
 }
@@ -314,6 +411,56 @@ __device__ __forceinline__ void cp_async16(const void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Wide passes: the sum-of-squares partials of every row (4 per 128-column
+// tile of the previous RESID phase) are staged into attention buffer 1 —
+// idle during GEMM phases — with cp.async as the phase starts, and reduced
+// with load_rstd's per-row tree (lane-strided sums, then the xor butterfly,
+// here transposed over 8 rows) when the first epilogue needs them.
+__device__ __forceinline__ int rstd_stage_ld(int rows) { return (rows + 3) & ~3; }
+__device__ __forceinline__ bool rstd_stage_fits(const MegaParams& P, const AttnSmem& A, int rows) {
+  return 4 * (P.H / 128) * rstd_stage_ld(rows) * 4 <= A.buf;
+}
+__device__ __forceinline__ void rstd_stage_issue(const MegaParams& P, const AttnSmem& A, int rows, int w, int lane) {
+  float* S = reinterpret_cast<float*>(A.K(1));
+  const int nparts = 4 * (P.H / 128), ld = rstd_stage_ld(rows);
+  for (int e = w; e < nparts; e += 4)
+    for (int v = 4 * lane; v < ld; v += 128) cp_async16(S + e * ld + v, P.ssq_part + size_t(e) * kMaxWindow + v);
+}
+__device__ __forceinline__ void rstd_stage_reduce(const MegaParams& P, const AttnSmem& A, int rows, int w, int lane,
+                                                  EpiSmem& es) {
+  const float* S = reinterpret_cast<const float*>(A.K(1));
+  const int nparts = 4 * (P.H / 128), ld = rstd_stage_ld(rows);
+  for (int g0 = w * 8; g0 < rows; g0 += 32) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = g0 + j;
+      a[j] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u;
+        a[j] += (e < nparts && t < rows) ? S[e * ld + t] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int step = 0; step < 3; ++step) {
+      const int half = 4 >> step;
+      const bool hi = (lane >> (4 - step)) & 1;
+#pragma unroll
+      for (int k = 0; k < half; ++k) {
+        const float send = hi ? a[k] : a[half + k];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 16 >> step);
+        if (hi) a[k] = a[half + k];
+        a[k] += recv;
+      }
+    }
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+    const int t = g0 + (lane >> 2);
+    if ((lane & 3) == 0 && t < rows) es.rstd[t] = 1.0f / sqrtf(a[0] / float(P.H) + P.eps);
+  }
+}
 
 struct AttnUnit {
   int t0, t1, kvh, s;
@@ -577,9 +724,13 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
 }
 
 
-// Partial slot of CTA cc's piece of `tile` (slot 0 = the CTA's first tile).
-__device__ __forceinline__ int piece_off(int cc, int tile, const Gemm& g, int m) {
-  return (cc * 2 + (sk_start(cc, g.G, g.T) / g.KB == tile ? 0 : 1)) * kMaxWindow * 128 + m;
+// Partial slot of a piece: slot 0 holds a CTA's first tile, slot 1 its last
+// (a CTA's middle tiles are whole and never stored). For the pieces of a
+// tile, every CTA after c_first starts its range inside the tile (slot 0);
+// c_first's piece is its first tile only when its range starts on the tile.
+__device__ __forceinline__ int piece_off_slot(int cc, int slot, int m) { return (cc * 2 + slot) * kMaxWindow * 128 + m; }
+__device__ __forceinline__ int first_piece_slot(int c_first, int tile, const Gemm& g) {
+  return sk_start(c_first, g.G, g.T) == tile * g.KB ? 0 : 1;
 }
 
 // Few-row passes (decode): a piece's partial is published as one 64-bit
@@ -606,19 +757,19 @@ __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int
                                               int lane, int c_first, int npieces, const Gemm& g, unsigned tag, float own,
                                               EpiSmem& es) {
   const unsigned long long* part = reinterpret_cast<const unsigned long long*>(P.part);
-  const bool resid = kind == PH_O || kind == PH_D;
-  float xo[1] = {resid ? __ldcg(P.x + tile * 128 + m) : 0.f};
+  EpiPre pre;
+  epi_load<1>(P, kind, 1, n0, tile, m, 0, pre);
   unsigned long long w[7];
 #pragma unroll
   for (int pc = 1; pc < 8; ++pc)
-    if (pc < npieces) w[pc - 1] = ld_tagged(part + piece_off(c_first + pc, tile, g, m));
+    if (pc < npieces) w[pc - 1] = ld_tagged(part + piece_off_slot(c_first + pc, 0, m));
   bool again = true;
   while (again) {
     again = false;
 #pragma unroll
     for (int pc = 1; pc < 8; ++pc)
       if (pc < npieces && unsigned(w[pc - 1] >> 32) != tag) {
-        w[pc - 1] = ld_tagged(part + piece_off(c_first + pc, tile, g, m));
+        w[pc - 1] = ld_tagged(part + piece_off_slot(c_first + pc, 0, m));
         again = true;
       }
   }
@@ -627,18 +778,23 @@ __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int
 #pragma unroll
   for (int pc = 1; pc < 8; ++pc)
     if (pc < npieces) v[0] += __uint_as_float(unsigned(w[pc - 1]));
-  finish_chunk<1>(P, kind, layer, 1, n0, tile, m, q, lane, 0, v, es, resid ? xo : nullptr);
+  finish_chunk<1>(P, kind, layer, 1, n0, tile, m, q, lane, 0, v, es, pre);
 }
 
 // Sum a split tile's piece partials (pieces = CTAs c_first.., in CTA order,
 // all loads in flight) for rows [r_lo, r_hi) and run the finishing math.
 __device__ __forceinline__ void finish_from_pieces(const MegaParams& P, int kind, int layer, int r_lo, int r_hi, int n0,
                                                    int tile, int m, int q, int lane, int c_first, int npieces,
-                                                   const Gemm& g, EpiSmem& es) {
+                                                   const Gemm& g, EpiSmem& es, int trace_p = -1) {
   int off[8];
 #pragma unroll
-  for (int pc = 0; pc < 8; ++pc) off[pc] = pc < npieces ? piece_off(c_first + pc, tile, g, m) : 0;
+  off[0] = piece_off_slot(c_first, first_piece_slot(c_first, tile, g), m);
+#pragma unroll
+  for (int pc = 1; pc < 8; ++pc) off[pc] = piece_off_slot(c_first + pc, 0, m);
+  if (trace_p >= 0 && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 3);
   for (int c0 = r_lo; c0 < r_hi; c0 += 8) {
+    EpiPre pre;
+    epi_load(P, kind, r_hi, n0, tile, m, c0, pre);
     float tmp[8][8];
 #pragma unroll
     for (int pc = 0; pc < 8; ++pc)
@@ -654,12 +810,26 @@ __device__ __forceinline__ void finish_from_pieces(const MegaParams& P, int kind
         if (pc < npieces) acc += tmp[pc][j];
       v[j] = acc;
     }
-    finish_chunk(P, kind, layer, r_hi, n0, tile, m, q, lane, c0, v, es);
+    if (trace_p >= 0 && c0 == r_lo && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
+    finish_chunk(P, kind, layer, r_hi, n0, tile, m, q, lane, c0, v, es, pre);
+    if (trace_p >= 0 && c0 == r_lo && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
   }
 }
 
+// A split tile this CTA finalises a row share of (wide passes).
+struct DefTile {
+  int tile, c_first, npieces, r_lo, r_hi, slot0;
+};
+
 }  // namespace
 
+// kWide: passes of more than one row (verify / prefill chunks / Jacobi
+// windows) — split tiles are finalised by all their pieces' CTAs (row shares
+// of fp32 partials). !kWide: 1-row decode steps — tagged single-word partials
+// and a fixed finaliser. Two instantiations keep each one's code and register
+// allocation free of the other's paths; the per-row arithmetic is the same
+// source, so a row is bitwise identical in both (tests/test_gpu_parity.py).
+template <bool kWide>
 __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ MegaParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t bars[2 * 8 + 4];
@@ -733,13 +903,20 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           const CUtensorMap* xm = xmap_of(P, kind);
           const int xrow = kind == PH_LM ? xrow_lm : 0;
           const uint32_t tx = kTileABytes + b_bytes;
-          const int pre = nk < ST ? nk : ST;
+          const int pre = min(min(nk, ST), P.pre_max);
           for (int i = 0; i < pre; ++i) {
             const uint32_t s = (it + i) % ST, ph = ((it + i) / ST) & 1;
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
             const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
             tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
+          }
+          // HBM is idle while the grid finishes the previous phase (its tail,
+          // and all of ATTN): the next P.pf[kind] boxes of this CTA's range
+          // beyond the ring go to L2 now, and the ring reads them from there
+          for (int i = pre; i < nk && i < pre + P.pf[kind]; ++i) {
+            const int x = po.block(i);
+            tma_prefetch_2d(wm, (x % g.KB) * kBK, (x / g.KB) * 128);
           }
           grid_wait(P.bar, unsigned(G) * unsigned(p - p_first + 1));  // activations of this phase are complete
           stamp(P, p, c, G, 0);
@@ -757,6 +934,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
             tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
           }
+          stamp(P, p, c, G, 12);
           it += nk;
         }
       }
@@ -795,7 +973,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             umma_commit(acc_full0 + 8 * b);
             ++acc_it;
           }
-          stamp(P, p, c, G, 3);
+          stamp(P, p, c, G, 13);
         }
       }
     }
@@ -857,16 +1035,32 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       }
       wk_bar();
       if (P.ctx->stop) break;
+      // wide passes: stage the RMSNorm partials now, reduce them at first use
+      bool rstd_pending = false;
+      if (kWide && !P.lm_only && (kind == PH_GU || kind == PH_LM || (kind == PH_QKV && layer > 0)) &&
+          rstd_stage_fits(P, A, rows)) {
+        rstd_stage_issue(P, A, rows, w, lane);
+        cp_async_commit();
+        rstd_pending = true;
+      }
       if (kind == PH_QKV) {
         // keys cached by earlier passes for this CTA's first attention unit of
         // the layer: requested now, consumed after the next barrier
         int un = 0;
         const AttnUnit U0 = attn_unit_from(P, rows, n0, c, G, un);
-        if (U0.valid) {
-          attn_issue(P, layer, U0, n0, A, 0, 0, tid);
-          cp_async_commit();
-        }
+        if (U0.valid) attn_issue(P, layer, U0, n0, A, 0, 0, tid);
+        if (U0.valid || rstd_pending) cp_async_commit();  // (the staged partials are the group before)
       }
+      auto ensure_rstd = [&]() {
+        if (!rstd_pending) return;
+        if (kind == PH_QKV) cp_async_wait<1>(); else cp_async_wait<0>();
+        wk_bar();
+        rstd_stage_reduce(P, A, rows, w, lane, es);
+        wk_bar();
+        if (kind == PH_LM && c == 0)
+          for (int t = tid; t < rows; t += kWorkers) P.rstd_cache[n0 + t] = es.rstd[t];
+        rstd_pending = false;
+      };
       if (kind == PH_FINAL) {
         // argmax of every row over the per-CTA partials of the LM phase;
         // rows are spread over CTAs (t = c, c+G, ...), one warp per row
@@ -933,7 +1127,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         if (P.lm_only) {  // LM head over resident rows: the final rstd of each position is cached
           for (int t = tid; t < rows; t += kWorkers) es.rstd[t] = P.rstd_cache[n0 + t];
           wk_bar();
-        } else if (kind == PH_QKV || kind == PH_GU || kind == PH_LM) {
+        } else if ((kind == PH_QKV || kind == PH_GU || kind == PH_LM) && !rstd_pending) {
           load_rstd(P, kind == PH_QKV && layer == 0, rows, w, lane, es);
           wk_bar();
           if (kind == PH_LM && c == 0)
@@ -947,7 +1141,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         // first-block CTA finalizes (finish_tagged). Wider passes (verify /
         // prefill): every piece publishes without blocking and counts in,
         // then each piece's CTA finalizes its own share of the rows.
-        const bool spread = rows > 1;
+        constexpr bool spread = kWide;
         int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
         if (kind == PH_LM) {
           for (int e = tid; e < 4 * kMaxWindow; e += kWorkers) {
@@ -975,10 +1169,16 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           if (tid == 0) stamp(P, p, c, G, 4);
           const uint32_t trow = tmem + b * uint32_t(P.acc_cols) + (uint32_t(q * 32) << 16);
           if (npieces == 1) {
+            ensure_rstd();
+            // the next chunk's per-row inputs are in flight while this one finishes
+            EpiPre cur, nxt;
+            epi_load(P, kind, rows, n0, tile, m, 0, cur);
             for (int c0 = 0; c0 < rows; c0 += 8) {
+              if (c0 + 8 < rows) epi_load(P, kind, rows, n0, tile, m, c0 + 8, nxt);
               float v[8];
               tmem_ld8(trow + c0, v);
-              finish_chunk(P, kind, layer, rows, n0, tile, m, q, lane, c0, v, es);
+              finish_chunk(P, kind, layer, rows, n0, tile, m, q, lane, c0, v, es, cur);
+              cur = nxt;
             }
             tc_fence_before();
             wk_bar();
@@ -992,7 +1192,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
             finish_tagged(P, kind, layer, n0, tile, m, q, lane, c_first, npieces, g, tag0 + unsigned(p), v[0], es);
           } else if (!spread) {
-            unsigned long long* mine = reinterpret_cast<unsigned long long*>(P.part) + piece_off(c, tile, g, m);
+            unsigned long long* mine = reinterpret_cast<unsigned long long*>(P.part) + piece_off_slot(c, pj == 0 ? 0 : 1, m);
             float v[8];
             tmem_ld8(trow, v);
             st_tagged(mine, tag0 + unsigned(p), v[0]);
@@ -1000,12 +1200,12 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             wk_bar();
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
           } else {
-            float* mine = P.part + piece_off(c, tile, g, m);
-            for (int c0 = 0; c0 < rows; c0 += 8) {
-              float v[8];
-              tmem_ld8(trow + c0, v);
+            float* mine = P.part + piece_off_slot(c, pj == 0 ? 0 : 1, m);
+            for (int c0 = 0; c0 < rows; c0 += 32) {
+              float v[32];
+              tmem_ld32(trow + c0, v);
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
+              for (int j = 0; j < 32; ++j)
                 if (c0 + j < rows) mine[size_t(c0 + j) * 128] = v[j];
             }
             tc_fence_before();
@@ -1026,26 +1226,33 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           (void)piece_hi;
         }
         if (tid == 0) stamp(P, p, c, G, 5);
-        // second pass (many rows): wait for each split tile's pieces, finalize this CTA's row share
-        for (int d = 0; d < 2; ++d) {
-          const int tile = d == 0 ? dtile0 : dtile1;
-          if (tile < 0) continue;
-          const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
-          const int npieces = c_last - c_first + 1, my_idx = c - c_first;
-          // spread: every piece's CTA takes a share of the rows; otherwise this
-          // CTA was the last arrival and finalises all rows
-          const int r_lo = spread ? my_idx * rows / npieces : 0;
-          const int r_hi = spread ? (my_idx + 1) * rows / npieces : rows;
-          if (spread) {
-            if (tid == 0) {
-              grid_wait(cnt + tile, unsigned(npieces));
-              if (d == 0) stamp(P, p, c, G, 7);
-            }
-            wk_bar();
+        ensure_rstd();  // (also completes the staging copies before the buffer is reused)
+        if constexpr (kWide) {
+          // second pass: wait for the split tiles' pieces, then finalise this
+          // CTA's row share of each (every piece's CTA takes a share)
+          auto def_of = [&](int tile) {
+            const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
+            const int npieces = c_last - c_first + 1, my_idx = c - c_first;
+            return DefTile{tile, c_first, npieces, my_idx * rows / npieces, (my_idx + 1) * rows / npieces,
+                           first_piece_slot(c_first, tile, g)};
+          };
+          // dtile1 is only set once dtile0 is
+          const int nd = (dtile0 >= 0) + (dtile1 >= 0);
+          DefTile D[2] = {dtile0 >= 0 ? def_of(dtile0) : DefTile{0, 0, 1, 0, 0, 0},
+                          dtile1 >= 0 ? def_of(dtile1) : DefTile{0, 0, 1, 0, 0, 0}};
+          if (tid == 0) {
+            if (nd > 0) grid_wait(cnt + D[0].tile, unsigned(D[0].npieces));
+            if (nd > 1) grid_wait(cnt + D[1].tile, unsigned(D[1].npieces));
+            stamp(P, p, c, G, 7);
           }
-          if (tid == 0 && d == 0) stamp(P, p, c, G, 8);
-          if (r_lo < r_hi) finish_from_pieces(P, kind, layer, r_lo, r_hi, n0, tile, m, q, lane, c_first, npieces, g, es);
-          if (tid == 0 && d == 0) stamp(P, p, c, G, 9);
+          wk_bar();
+          if (tid == 0) stamp(P, p, c, G, 8);
+#pragma unroll
+          for (int d = 0; d < 2; ++d)
+            if (d < nd && D[d].r_lo < D[d].r_hi)
+              finish_from_pieces(P, kind, layer, D[d].r_lo, D[d].r_hi, n0, D[d].tile, m, q, lane, D[d].c_first,
+                                 D[d].npieces, g, es, d == 0 ? p : -1);
+          if (tid == 0) stamp(P, p, c, G, 9);
         }
         if (tid == 0) stamp(P, p, c, G, 6);
         if (kind == PH_LM) {
@@ -1080,8 +1287,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
 int mega_static_smem() {
   static int static_smem = -1;
   if (static_smem < 0) {
-    cudaFuncAttributes fa{};
-    static_smem = cudaFuncGetAttributes(&fa, mega_kernel) == cudaSuccess ? int(fa.sharedSizeBytes) : 16 * 1024;
+    cudaFuncAttributes fa{}, fb{};
+    static_smem = cudaFuncGetAttributes(&fa, mega_kernel<false>) == cudaSuccess &&
+                          cudaFuncGetAttributes(&fb, mega_kernel<true>) == cudaSuccess
+                      ? int(fa.sharedSizeBytes > fb.sharedSizeBytes ? fa.sharedSizeBytes : fb.sharedSizeBytes)
+                      : 16 * 1024;
   }
   return static_smem;
 }
@@ -1090,9 +1300,12 @@ int mega_static_smem() {
 // handles created later never shrink it under a running configuration.
 cudaError_t mega_set_smem_attr() {
   static cudaError_t done = cudaErrorNotReady;
-  if (done == cudaErrorNotReady)
-    done = cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024 - mega_static_smem());
+  if (done == cudaErrorNotReady) {
+    const int bytes = 227 * 1024 - mega_static_smem();
+    done = cudaFuncSetAttribute(mega_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (done == cudaSuccess)
+      done = cudaFuncSetAttribute(mega_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
   return done;
 }
 
@@ -1110,7 +1323,7 @@ int mega_smem_bytes(int ntok, int stages, int attn_floats) {
   return stages * (kTileABytes + ntok * 128) + attn_floats * 4 + 1024;
 }
 
-cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st) {
+cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cudaStream_t st) {
   if (const cudaError_t e = mega_set_smem_attr(); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1122,14 +1335,17 @@ cudaError_t launch_mega(const MegaParams& P, int grid, int smem, cudaStream_t st
   attr1[0].val.cooperative = 1;
   cfg.attrs = attr1;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mega_kernel, P);
+  return wide ? cudaLaunchKernelEx(&cfg, mega_kernel<true>, P) : cudaLaunchKernelEx(&cfg, mega_kernel<false>, P);
 }
 
 int mega_max_blocks_per_sm(int smem) {
   if (mega_set_smem_attr() != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel, 192, smem) != cudaSuccess) return 0;
-  return n;
+  int n2 = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<false>, 192, smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, mega_kernel<true>, 192, smem) != cudaSuccess)
+    return 0;
+  return n < n2 ? n : n2;
 }
 
 }  // namespace ps

@@ -418,6 +418,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.tok_in = tok_in;
   P.L = h->L; P.H = h->H; P.qd = h->qd; P.kvd = h->kvd; P.I = h->I; P.hd = h->hd;
   P.heads = h->nh; P.kv_heads = h->nkv; P.vocab_local = h->v_count; P.v_begin = h->v_begin;
+  P.hd_shift = h->hd == 128 ? 7 : 6;
   P.ntok = ntok;
   P.stages = mega_stages(ntok, attn_floats);
   int cols = 32;
@@ -463,9 +464,31 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.logits_out = logits_out;
   P.ld_logits = h->v_count;
   P.trace = h->mega_trace;
+  {
+    // L2 prefetch depth (weight boxes per CTA beyond the smem ring) for the
+    // phases QKV, O, GU, D, LM; PS_PF_DECODE / PS_PF_WIDE="q:o:gu:d:lm" override
+    static int pf_dec[5] = {0, 0, 0, 0, 0}, pf_wide[5] = {0, 0, 0, 0, 0};
+    static bool pf_init = false;
+    if (!pf_init) {
+      if (const char* e = std::getenv("PS_PF_DECODE"))
+        std::sscanf(e, "%d:%d:%d:%d:%d", &pf_dec[0], &pf_dec[1], &pf_dec[2], &pf_dec[3], &pf_dec[4]);
+      if (const char* e = std::getenv("PS_PF_WIDE"))
+        std::sscanf(e, "%d:%d:%d:%d:%d", &pf_wide[0], &pf_wide[1], &pf_wide[2], &pf_wide[3], &pf_wide[4]);
+      pf_init = true;
+    }
+    const int* pf = max_rows > 1 ? pf_wide : pf_dec;
+    static int pre_dec = 8, pre_wide = 8;
+    static bool pre_init = false;
+    if (!pre_init) {
+      if (const char* e = std::getenv("PS_PRE")) std::sscanf(e, "%d:%d", &pre_dec, &pre_wide);
+      pre_init = true;
+    }
+    P.pre_max = max_rows > 1 ? pre_wide : pre_dec;
+    for (int k = 0; k < 5; ++k) P.pf[1 + (k == 0 ? 0 : k + 1)] = pf[k];  // kinds QKV=1, O=3, GU=4, D=5, LM=6
+  }
   cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned) * h->mega_cnt_words, h->st);
   prof_mark(h, 7);
-  const cudaError_t e = launch_mega(P, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
+  const cudaError_t e = launch_mega(P, max_rows > 1, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
   if (e != cudaSuccess) std::fprintf(stderr, "predgen_b200: megakernel launch failed: %s\n", cudaGetErrorString(e));
   if (sharded && !lm_only) enqueue_shard_merge(h, ctx, max_rows, decode);
   prof_mark(h, 6);
@@ -839,7 +862,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
     if (!h->mega_part || !h->mega_epoch || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
     if (const char* tr = std::getenv("PS_TRACE"); tr && tr[0] == '1')
-      h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 12);
+      h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 16);
     std::vector<CUtensorMap> wm(size_t(4) * h->L + 1);
     for (int l = 0; l < h->L; ++l) {
       std::memcpy(&wm[4 * l + 0], h->layers[l].qkv.tm.bytes, sizeof(CUtensorMap));
@@ -1235,7 +1258,7 @@ int ps_trace(ps_handle* h, uint64_t* out, int64_t cap, int32_t* nphases, int32_t
   if (!h->mega_trace) return fail(PS_ERR_INVALID, "tracing is off (set PS_TRACE=1 before ps_create)");
   *nphases = 3 + 5 * h->L;
   *ctas = h->sms;
-  const int64_t n = int64_t(*nphases) * h->sms * 12;
+  const int64_t n = int64_t(*nphases) * h->sms * 16;
   if (out) CK(cudaMemcpy(out, h->mega_trace, sizeof(uint64_t) * std::min<int64_t>(cap, n), cudaMemcpyDeviceToHost));
   return PS_OK;
 }

@@ -14,7 +14,7 @@ lm.forward(toks)
 for rep in range(3):
     lm.discard_after(len(toks))
     steps = lm.decode_greedy_fused(toks, 3)
-NS = 12
+NS = 16
 names = ["EMB"] + [k for l in range(shape.layers) for k in ("QKV", "ATT", "O", "GU", "D")] + ["LM", "FIN"]
 
 def grab():
@@ -33,7 +33,7 @@ def report(tr, label):
         start = np.nanmax(tr[p - 1, :, 2])
         a = agg[names[p]]
         a["span"].append(np.nanmax(tr[p, :, 2]) - start)
-        for slot, key in ((1, "bar"), (4, "acc_last"), (5, "published"), (7, "waited|a_start"), (8, "a_loaded"), (9, "a_computed"), (10, "a_counted"), (11, "a_merged"), (6, "deferred")):
+        for slot, key in ((0, "prod_bar"), (12, "prod_done"), (13, "mma_done"), (1, "bar"), (3, "offs"), (4, "acc_last"), (5, "published"), (7, "waited|a_start"), (8, "a_loaded"), (9, "a_computed"), (10, "a_counted"), (11, "a_merged"), (6, "deferred")):
             col = tr[p, :, slot]
             if np.isfinite(col).any():
                 a[key + "_max"].append(np.nanmax(col) - start)
