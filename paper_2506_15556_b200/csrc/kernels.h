@@ -158,6 +158,7 @@ struct MegaParams {
   int* am_idx;
   unsigned long long* keys;
   unsigned* bar;            // grid barrier counter, zeroed before launch
+  unsigned* bar2;           // wide passes: attention-merge sync counter (one arrival per CTA per layer)
   int lm_only;              // 1: LM head + argmax over resident rows [n0, n0+rows) only (hn / rstd caches)
   float* logits_out;        // optional fp32 logits [rows][ld_logits] from the LM epilogue
   int ld_logits;
@@ -167,7 +168,16 @@ struct MegaParams {
 };
 // attention staging of the megakernel (see AttnSmem in megakernel.cu): two
 // unit buffers of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
-inline int mega_attn_bytes(int hd, int grp) { return 2 * (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2); }
+// wide passes: K and V only (q fragments are read from global memory); a
+// buffer also holds the staged RMSNorm partials of up to kRstdStageRows rows
+constexpr int kRstdStageRows = 80;
+__host__ __device__ inline int mega_attn_buf_wide(int hd, int H) {
+  const int kv = 2 * kPage * (hd + 8) * 2, rs = 4 * (H / 128) * kRstdStageRows * 4;
+  return kv > rs ? kv : rs;
+}
+inline int mega_attn_bytes(int hd, int grp, bool wide, int H) {
+  return wide ? 2 * mega_attn_buf_wide(hd, H) : 2 * (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2);
+}
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);
 // wide: the pass may have more than one row (max_rows > 1)

@@ -135,6 +135,14 @@ __device__ __forceinline__ const CUtensorMap* xmap_of(const MegaParams& P, int k
   return P.xmaps + (kind == PH_O ? 1 : kind == PH_D ? 2 : kind == PH_LM ? 3 : 0);
 }
 
+// 2^x on the SFU (ex2.approx.ftz: one MUFU op; 2^-inf = 0, results below
+// 2^-126 flush to 0 — negligible softmax weights)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ---------------------------------------------------------------------------
 // epilogue math for one finished 8-column chunk of tile rows [128*tile, +128)
 struct EpiSmem {
@@ -144,7 +152,8 @@ struct EpiSmem {
   int red_i[4][8];
   float rstd[kMaxWindow];
   int flag;
-  int rflag[8];
+  int rflag[32 * 4];  // [unit][row] of the ATT phase's deferred unit list
+  int ulist[32][4];   // (t0, t1, kv head, page) of units computed, not yet counted
 };
 
 // Barrier-free: every warp finishes its own 32 rows. RoPE / SwiGLU partners
@@ -229,7 +238,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       const float val = t < rows ? v[j] * es.rstd[t] : 0.f;
       const float up = __shfl_xor_sync(0xffffffffu, val, 1);
       if (t < rows && (m & 1) == 0)
-        P.act[size_t(t) * P.I + tile * 64 + (m >> 1)] = __float2bfloat16_rn(val / (1.0f + expf(-val)) * up);
+        P.act[size_t(t) * P.I + tile * 64 + (m >> 1)] = __float2bfloat16_rn(__fdividef(val, 1.0f + ex2(val * -1.4426950408889634f)) * up);
     }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
@@ -380,6 +389,8 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
 // still in the layer's QKV phase, only this pass's rows (and q) after the
 // barrier, and unit i+1's loads overlap unit i's math.
 constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
+constexpr int kMaxUnitList = 32;  // units computed before their counts/merges are flushed
+constexpr int kAttnRowsW = 16;    // wide passes: query rows per unit (one 4-row M-tile per worker warp)
 
 struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf
   unsigned char* base;
@@ -396,12 +407,14 @@ struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf
   }
 };
 
-__device__ __forceinline__ AttnSmem attn_smem(void* base, int hd, int grp) {
+// wide passes stage no q (fragments come from global memory) but reuse a
+// buffer for the RMSNorm partials of up to kRstdStageRows rows
+__device__ __forceinline__ AttnSmem attn_smem(void* base, int hd, int grp, bool wide, int H) {
   AttnSmem a;
   a.base = static_cast<unsigned char*>(base);
   a.koff_v = kPage * (hd + 8) * 2;
   a.koff_q = 2 * a.koff_v;
-  a.buf = a.koff_q + kAttnRows * grp * (hd + 8) * 2;
+  a.buf = wide ? mega_attn_buf_wide(hd, H) : a.koff_q + kAttnRows * grp * (hd + 8) * 2;
   return a;
 }
 
@@ -469,14 +482,15 @@ struct AttnUnit {
 
 // The i-th unit (i >= 0 counts only units with work) of CTA c: units are
 // dealt round-robin (u = c, c + G, ...), page fastest.
+template <int R>
 __device__ __forceinline__ AttnUnit attn_unit_from(const MegaParams& P, int rows, int n0, int u_start, int G, int& u_next) {
   const int npages = (n0 + rows - 1) / kPage + 1;
-  const int nblocks = (rows + kAttnRows - 1) / kAttnRows;
+  const int nblocks = (rows + R - 1) / R;
   const int units = nblocks * P.kv_heads * npages;
   AttnUnit U{0, 0, 0, 0, false};
   for (int u = u_start; u < units; u += G) {
     const int s = u % npages, r = u / npages;
-    const int t0 = (r / P.kv_heads) * kAttnRows, t1 = min(rows, t0 + kAttnRows);
+    const int t0 = (r / P.kv_heads) * R, t1 = min(rows, t0 + R);
     if (s > (n0 + t1 - 1) / kPage) continue;  // no row of the block reaches this page
     U = AttnUnit{t0, t1, r % P.kv_heads, s, true};
     u_next = u + G;
@@ -488,6 +502,7 @@ __device__ __forceinline__ AttnUnit attn_unit_from(const MegaParams& P, int rows
 
 // Request a unit's operands into buffer b: part 0 = keys written by earlier
 // passes (positions < n0), part 1 = this pass's keys and the q rows.
+template <bool kWide>
 __device__ __forceinline__ void attn_issue(const MegaParams& P, int layer, const AttnUnit& U, int n0, const AttnSmem& A,
                                            int b, int part, int tid) {
   const int hd = P.hd, grp = P.heads / P.kv_heads, vpr = hd / 8;
@@ -509,7 +524,7 @@ __device__ __forceinline__ void attn_issue(const MegaParams& P, int layer, const
       *reinterpret_cast<uint4*>(A.V(b) + j * (hd + 8) + d0) = make_uint4(0u, 0u, 0u, 0u);
     }
     const int qvec_row = grp * hd / 8;
-    for (int e = tid; e < (U.t1 - U.t0) * qvec_row; e += kWorkers) {
+    for (int e = tid; !kWide && e < (U.t1 - U.t0) * qvec_row; e += kWorkers) {
       const int r = e / qvec_row, rem = (e % qvec_row) * 8;
       // pair (r, head) -> Q row r * grp + head
       cp_async16(A.Q(b) + (r * grp + rem / hd) * (hd + 8) + rem % hd,
@@ -541,7 +556,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // pair sits in the tile, so 1-row decode and wide verify agree bitwise.
 // Then the page arrival count and, for rows whose last page this was, the merge.
 __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUnit& U, int n0, const AttnSmem& A, int b,
-                                               int w, int lane, int* rflag, int trace_p = -1) {
+                                               int w, int lane, int trace_p = -1) {
   const bool tr = trace_p >= 0 && threadIdx.x == 64;
   const int hd = P.hd, grp = P.heads / P.kv_heads;
   const int t0 = U.t0, t1 = U.t1, kvh = U.kvh, s = U.s;
@@ -549,28 +564,40 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
   const int nrows = t1 - t0;
   const int npairs = nrows * grp;
   const int ld = (hd + 8) / 2;  // row stride in 32-bit words
-  const uint32_t* Q32 = reinterpret_cast<const uint32_t*>(A.Q(b));
-  const uint32_t* K32 = reinterpret_cast<const uint32_t*>(A.K(b));
+  const uint32_t qbase = smem_u32(A.Q(b)), kbase = smem_u32(A.K(b));
   const uint32_t vbase = smem_u32(A.V(b));
+  const uint32_t rs = uint32_t(hd + 8) * 2;  // staged row stride in bytes (conflict-free ldmatrix phases)
+  // log2-domain softmax: v = s * scale * log2(e), p = 2^(v - max)
+  const float sl2 = P.attn_scale * 1.4426950408889634f;
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 8);
   const int g8 = lane >> 2, q4 = lane & 3;
+  const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: this lane addresses row mr of matrix mi
   for (int mt = 0; mt * 16 < npairs; ++mt) {
     const int p0 = mt * 16 + g8, p1 = p0 + 8;
-    const bool in0 = p0 < npairs, in1 = p1 < npairs;
-    // ---- S = Q K^T for 16 pairs x 64 keys
+    // ---- S = Q K^T for 16 pairs x 64 keys. Fragments by ldmatrix; rows of
+    // the tile past npairs hold stale data, which only reaches their own
+    // (masked, never stored) rows.
     float S[8][4];
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) S[nt][0] = S[nt][1] = S[nt][2] = S[nt][3] = 0.f;
+    const uint32_t qa = qbase + uint32_t(mt * 16 + (mi & 1) * 8 + mr) * rs + uint32_t(mi >> 1) * 16;
+    const uint32_t ka = kbase + uint32_t((mi >> 1) * 8 + mr) * rs + uint32_t(mi & 1) * 16;
     for (int ks = 0; ks < hd / 16; ++ks) {
-      const int kw = ks * 8 + q4;  // word column of this lane's first two dims
-      const uint32_t a0 = in0 ? Q32[p0 * ld + kw] : 0u, a1 = in1 ? Q32[p1 * ld + kw] : 0u;
-      const uint32_t a2 = in0 ? Q32[p0 * ld + kw + 4] : 0u, a3 = in1 ? Q32[p1 * ld + kw + 4] : 0u;
+      uint32_t a0, a1, a2, a3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                   : "r"(qa + ks * 32));
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const uint32_t* kr = K32 + (nt * 8 + g8) * ld + kw;
-        mma_bf16(S[nt], a0, a1, a2, a3, kr[0], kr[4]);
+      for (int nt = 0; nt < 8; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(ka + uint32_t(nt * 8) * rs + ks * 32));
+        mma_bf16(S[nt], a0, a1, a2, a3, b0, b1);
+        mma_bf16(S[nt + 1], a0, a1, a2, a3, b2, b3);
       }
     }
+    if (tr && mt == 0) { float z = S[0][0] + S[7][3]; if (z == 12345.f) stamp(P, trace_p, blockIdx.x, gridDim.x, 15); stamp(P, trace_p, blockIdx.x, gridDim.x, 14); }
     // ---- causal mask + page-local softmax; rows p0 (S[.][0..1]) and p1 (S[.][2..3])
     int nk[2];
     float mx[2], l[2];
@@ -585,7 +612,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int key = nt * 8 + q4 * 2 + e;
-          const float v = key < nk[h] ? S[nt][2 * h + e] * P.attn_scale : -INFINITY;
+          const float v = key < nk[h] ? S[nt][2 * h + e] * sl2 : -INFINITY;
           S[nt][2 * h + e] = v;
           m = fmaxf(m, v);
         }
@@ -597,7 +624,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const float pv = nk[h] > 0 ? expf(S[nt][2 * h + e] - m) : 0.f;  // exp(-inf) = 0 past the mask
+          const float pv = nk[h] > 0 ? ex2(S[nt][2 * h + e] - m) : 0.f;  // 2^(-inf) = 0 past the mask
           S[nt][2 * h + e] = pv;
           sum += pv;
         }
@@ -606,6 +633,7 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
       mx[h] = m;
       l[h] = sum;
     }
+    if (tr && mt == 0) { float z = l[0] + l[1]; if (z == 12345.f) stamp(P, trace_p, blockIdx.x, gridDim.x, 14); stamp(P, trace_p, blockIdx.x, gridDim.x, 15); }
     // ---- O = P V for this warp's quarter of the head dims (n-tiles of 8)
     const int ndt = hd / 32;  // dim tiles per warp
     float O[4][4];
@@ -660,67 +688,289 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
   }
   wk_bar();
   if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 9);
-  // page arrival for every row of the block at once; the last page merges
-  if (tid < nrows) {
-    const int t = t0 + tid, pos = n0 + t;
-    rflag[tid] = 0;
-    if (s <= pos / kPage) {
-      unsigned* cnt = P.acnt + size_t(t) * P.kv_heads + kvh;
-      const unsigned old = atom_add_acq_rel(cnt, 1u);
-      if (old == unsigned(pos / kPage)) {
-        rflag[tid] = 1;
-        *cnt = 0u;
+}
+
+// Wide passes: unit = (kv head, page, block of kAttnRowsW rows); worker warp
+// w owns the M-tile of rows t0+4w .. +3 (x grp heads) and computes its S,
+// page-local softmax and P.V over all head dims. q fragments come straight
+// from global memory (L2); K and V are staged in buffer b. The per-pair
+// operation sequence (fragment values, MMA order over k-steps and key steps,
+// softmax, hi/lo P) is attention_unit's, so results are bitwise the decode
+// step's. Page-local (O, m, l) go to o_part / ml_part; the merge runs after
+// a grid-wide sync (attn_merge_items).
+__device__ __forceinline__ void attention_unit_wide(const MegaParams& P, const AttnUnit& U, int n0, const AttnSmem& A,
+                                                    int b, int w, int lane) {
+  const int hd = P.hd, grp = P.heads / P.kv_heads;
+  const int r0 = U.t0 + 4 * w;
+  const int nr = min(4, U.t1 - r0);
+  if (nr <= 0) return;
+  const int npairs = nr * grp;
+  const int s = U.s, kvh = U.kvh;
+  const uint32_t kbase = smem_u32(A.K(b)), vbase = smem_u32(A.V(b));
+  const uint32_t rs = uint32_t(hd + 8) * 2;
+  const float sl2 = P.attn_scale * 1.4426950408889634f;
+  const int g8 = lane >> 2, q4 = lane & 3;
+  const int mi = lane >> 3, mr = lane & 7;
+  const int p0 = g8, p1 = g8 + 8;
+  // q fragments of pairs p0 / p1 (zero past npairs), all k-steps up front
+  uint32_t qf[8][4];
+  {
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p0 / grp) * P.qd +
+                                                           size_t(kvh * grp + p0 % grp) * hd) + q4;
+    const uint32_t* qb = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p1 / grp) * P.qd +
+                                                           size_t(kvh * grp + p1 % grp) * hd) + q4;
+    const bool va = p0 < npairs, vb = p1 < npairs;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const bool k_ok = ks < hd / 16;
+      qf[ks][0] = (va && k_ok) ? __ldcg(qa + ks * 8) : 0u;
+      qf[ks][1] = (vb && k_ok) ? __ldcg(qb + ks * 8) : 0u;
+      qf[ks][2] = (va && k_ok) ? __ldcg(qa + ks * 8 + 4) : 0u;
+      qf[ks][3] = (vb && k_ok) ? __ldcg(qb + ks * 8 + 4) : 0u;
+    }
+  }
+  float S[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) S[nt][0] = S[nt][1] = S[nt][2] = S[nt][3] = 0.f;
+  const uint32_t ka = kbase + uint32_t((mi >> 1) * 8 + mr) * rs + uint32_t(mi & 1) * 16;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    if (ks < hd / 16) {
+#pragma unroll
+      for (int nt = 0; nt < 8; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(ka + uint32_t(nt * 8) * rs + ks * 32));
+        mma_bf16(S[nt], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
+        mma_bf16(S[nt + 1], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b2, b3);
       }
     }
   }
-  wk_bar();
-  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
-  // merge, one warp per (row, head): lane sp owns page sp for the scalars
-  // (fixed butterfly); the output sums run over pages in order, loads batched
-  for (int it = w; it < nrows * grp; it += 4) {
-    const int r = it / grp, hh = it % grp;
-    if (!rflag[r]) continue;
-    const int t = t0 + r, pos = n0 + t;
-    const int nsplit = pos / kPage + 1;
-    const int h = kvh * grp + hh;
-    const size_t base = (size_t(t) * P.heads + h) * P.max_splits_attn;
-    float M = -INFINITY;
-    for (int sp = lane; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
-    M = warp_max(M);
-    float Lp = 0.f;
-    for (int sp = lane; sp < nsplit; sp += 32)
-      Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * expf(__ldcg(P.ml_part + (base + sp) * 2) - M);
-    const float L = warp_sum(Lp);
-    for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int sp0 = 0; sp0 < nsplit; sp0 += 8) {
-        float mv[8];
-        float4 o[8];
+  int nk[2];
+  float mx[2], l[2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (sp0 + u < nsplit) {
-            mv[u] = __ldcg(P.ml_part + (base + sp0 + u) * 2);
-            o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp0 + u) * hd + d4));
-          }
+  for (int h = 0; h < 2; ++h) {
+    const int pp = h ? p1 : p0;
+    const int pos = n0 + r0 + pp / grp;
+    nk[h] = (pp < npairs) ? min(kPage, pos + 1 - s * kPage) : 0;
+    float m = -INFINITY;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (sp0 + u < nsplit) {
-            const float f = expf(mv[u] - M);
-            acc.x = fmaf(o[u].x, f, acc.x);
-            acc.y = fmaf(o[u].y, f, acc.y);
-            acc.z = fmaf(o[u].z, f, acc.z);
-            acc.w = fmaf(o[u].w, f, acc.w);
-          }
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = nt * 8 + q4 * 2 + e;
+        const float v = key < nk[h] ? S[nt][2 * h + e] * sl2 : -INFINITY;
+        S[nt][2 * h + e] = v;
+        m = fmaxf(m, v);
       }
-      __nv_bfloat16* dst = P.attn + size_t(t) * P.qd + size_t(h) * hd + d4;
-      dst[0] = __float2bfloat16_rn(acc.x / L);
-      dst[1] = __float2bfloat16_rn(acc.y / L);
-      dst[2] = __float2bfloat16_rn(acc.z / L);
-      dst[3] = __float2bfloat16_rn(acc.w / L);
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if (nk[h] <= 0) m = 0.f;
+    float sum = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float pv = nk[h] > 0 ? ex2(S[nt][2 * h + e] - m) : 0.f;
+        S[nt][2 * h + e] = pv;
+        sum += pv;
+      }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    mx[h] = m;
+    l[h] = sum;
+  }
+  // P as bf16 hi + lo fragments, per 16-key step
+  uint32_t ah[4][4], al[4][4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const float* x0 = S[2 * kk];
+    const float* x1 = S[2 * kk + 1];
+    const float src[4][2] = {{x0[0], x0[1]}, {x0[2], x0[3]}, {x1[0], x1[1]}, {x1[2], x1[3]}};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(src[i][0], src[i][1]);
+      const float2 hf = __bfloat1622float2(hi);
+      ah[kk][i] = *reinterpret_cast<const uint32_t*>(&hi);
+      al[kk][i] = pack_bf16(src[i][0] - hf.x, src[i][1] - hf.y);
     }
   }
+  size_t slot[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int pp = h ? p1 : p0;
+    slot[h] = (size_t(r0 + pp / grp) * P.heads + kvh * grp + pp % grp) * P.max_splits_attn + s;
+  }
+  // O = P V over the head dims, 8 dim tiles (64 dims) at a time
+  for (int d0 = 0; d0 < hd / 8; d0 += 8) {
+    float O[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t addr = vbase + uint32_t(((kk * 16 + (lane & 15)) * (hd + 8) + (d0 + i) * 8) * 2);
+        uint32_t b0, b1;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(addr));
+        mma_bf16(O[i], ah[kk][0], ah[kk][1], ah[kk][2], ah[kk][3], b0, b1);
+        mma_bf16(O[i], al[kk][0], al[kk][1], al[kk][2], al[kk][3], b0, b1);
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (nk[h] <= 0) continue;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float2*>(P.o_part + slot[h] * hd + (d0 + i) * 8 + q4 * 2) =
+            make_float2(O[i][2 * h], O[i][2 * h + 1]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (nk[h] > 0 && q4 == 0) {
+      P.ml_part[slot[h] * 2] = mx[h];
+      P.ml_part[slot[h] * 2 + 1] = l[h];
+    }
+}
+
+// One (row, head) merge by a whole warp. Lane sp owns page sp's (m, l): M is
+// the warp max, L the butterfly sum of l * 2^(m - M); the output sums run over
+// pages in order, lane d owning dims 4d..4d+3. The first 8 pages' operands
+// are requested up front (MergeLoad), so a merge over up to 512 tokens costs
+// one memory round trip; two items per warp overlap theirs.
+struct MergeLoad {
+  float2 ml;     // (m, l) of page `lane` (lane < nsplit)
+  float4 o[8];   // dims 4*lane.. of pages 0..7
+  int t, h, nsplit;
+  size_t base;
+};
+
+__device__ __forceinline__ void attn_merge_load(const MegaParams& P, int n0, int t, int h, int lane, MergeLoad& L) {
+  const int hd = P.hd;
+  L.t = t;
+  L.h = h;
+  L.nsplit = (n0 + t) / kPage + 1;
+  L.base = (size_t(t) * P.heads + h) * P.max_splits_attn;
+  L.ml = lane < L.nsplit ? __ldcg(reinterpret_cast<const float2*>(P.ml_part) + L.base + lane)
+                         : make_float2(-INFINITY, 0.f);
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (u < L.nsplit && lane * 4 < hd)
+      L.o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (L.base + u) * hd + lane * 4));
+}
+
+// Any context length: pages beyond the first 8 / 32 are streamed in batches.
+__device__ __forceinline__ void attn_merge_general(const MegaParams& P, int lane, const MergeLoad& L) {
+  const int hd = P.hd, nsplit = L.nsplit;
+  const size_t base = L.base;
+  float M = L.ml.x;
+  for (int sp = lane + 32; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(P.ml_part + (base + sp) * 2));
+  M = warp_max(M);
+  float Lp = 0.f;
+  if (lane < nsplit) Lp += L.ml.y * ex2(L.ml.x - M);
+  for (int sp = lane + 32; sp < nsplit; sp += 32)
+    Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * ex2(__ldcg(P.ml_part + (base + sp) * 2) - M);
+  const float Ls = warp_sum(Lp);
+  for (int d4 = lane * 4; d4 < hd; d4 += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp0 = 0; sp0 < nsplit; sp0 += 8) {
+      float f[8];
+      float4 o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (sp0 + u < nsplit) {
+          f[u] = ex2(__ldcg(P.ml_part + (base + sp0 + u) * 2) - M);
+          o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp0 + u) * hd + d4));
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (sp0 + u < nsplit) {
+          acc.x = fmaf(o[u].x, f[u], acc.x);
+          acc.y = fmaf(o[u].y, f[u], acc.y);
+          acc.z = fmaf(o[u].z, f[u], acc.z);
+          acc.w = fmaf(o[u].w, f[u], acc.w);
+        }
+    }
+    __nv_bfloat16* dst = P.attn + size_t(L.t) * P.qd + size_t(L.h) * hd + d4;
+    dst[0] = __float2bfloat16_rn(acc.x / Ls);
+    dst[1] = __float2bfloat16_rn(acc.y / Ls);
+    dst[2] = __float2bfloat16_rn(acc.z / Ls);
+    dst[3] = __float2bfloat16_rn(acc.w / Ls);
+  }
+}
+
+// The same arithmetic from the preloaded operands when nsplit <= 8, hd <= 128.
+__device__ __forceinline__ void attn_merge_finish(const MegaParams& P, int lane, const MergeLoad& L) {
+  const int hd = P.hd, nsplit = L.nsplit;
+  if (nsplit > 8 || hd > 128) {
+    attn_merge_general(P, lane, L);
+    return;
+  }
+  const float M = warp_max(L.ml.x);
+  float Lp = 0.f;
+  if (lane < nsplit) Lp += L.ml.y * ex2(L.ml.x - M);
+  const float Ls = warp_sum(Lp);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float f = ex2(__shfl_sync(0xffffffffu, L.ml.x, u) - M);
+    if (u < nsplit) {
+      acc.x = fmaf(L.o[u].x, f, acc.x);
+      acc.y = fmaf(L.o[u].y, f, acc.y);
+      acc.z = fmaf(L.o[u].z, f, acc.z);
+      acc.w = fmaf(L.o[u].w, f, acc.w);
+    }
+  }
+  if (lane * 4 < hd) {
+    __nv_bfloat16* dst = P.attn + size_t(L.t) * P.qd + size_t(L.h) * hd + lane * 4;
+    dst[0] = __float2bfloat16_rn(acc.x / Ls);
+    dst[1] = __float2bfloat16_rn(acc.y / Ls);
+    dst[2] = __float2bfloat16_rn(acc.z / Ls);
+    dst[3] = __float2bfloat16_rn(acc.w / Ls);
+  }
+}
+
+__device__ __forceinline__ void attn_merge_one(const MegaParams& P, int n0, int t, int h, int lane) {
+  MergeLoad L;
+  attn_merge_load(P, n0, t, h, lane, L);
+  attn_merge_finish(P, lane, L);
+}
+
+// Page arrival counts, then merges, for the units this CTA computed (deferred
+// so the unit loop runs math back to back). Thread (unit k, row r) counts;
+// the last page of a (row, kv head) merges its grp heads, one warp per (row,
+// head): lane sp owns page sp for the scalars (fixed butterfly); the output
+// sums run over pages in order, loads batched.
+__device__ __forceinline__ void attn_count_merge(const MegaParams& P, int n0, int nunits, int w, int lane, EpiSmem& es) {
+  const int tid = threadIdx.x - 64;
+  const int hd = P.hd, grp = P.heads / P.kv_heads;
+  if (tid < nunits * kAttnRows) {
+    const int k = tid / kAttnRows, r = tid % kAttnRows;
+    const int t0 = es.ulist[k][0], t1 = es.ulist[k][1], kvh = es.ulist[k][2], s = es.ulist[k][3];
+    int f = 0;
+    if (t0 + r < t1) {
+      const int t = t0 + r, pos = n0 + t;
+      if (s <= pos / kPage) {
+        unsigned* cnt = P.acnt + size_t(t) * P.kv_heads + kvh;
+        const unsigned old = atom_add_acq_rel(cnt, 1u);
+        if (old == unsigned(pos / kPage)) {
+          f = 1;
+          *cnt = 0u;
+        }
+      }
+    }
+    es.rflag[tid] = f;
+  }
   wk_bar();
-  if (tr) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
+  for (int it = w; it < nunits * kAttnRows * grp; it += 4) {
+    const int kr = it / grp, hh = it % grp;
+    if (!es.rflag[kr]) continue;
+    const int k = kr / kAttnRows;
+    const int t = es.ulist[k][0] + kr % kAttnRows, kvh = es.ulist[k][2];
+    attn_merge_one(P, n0, t, kvh * grp + hh, lane);
+  }
+  wk_bar();
 }
 
 
@@ -846,7 +1096,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   const int b_bytes = P.ntok * 128;
   auto a_tile = [&](int s) { return base + size_t(s) * (kTileABytes + b_bytes); };
   auto b_tile = [&](int s) { return a_tile(s) + kTileABytes; };
-  const AttnSmem A = attn_smem(base + size_t(ST) * (kTileABytes + b_bytes), P.hd, P.heads / P.kv_heads);
+  const AttnSmem A = attn_smem(base + size_t(ST) * (kTileABytes + b_bytes), P.hd, P.heads / P.kv_heads, kWide, P.H);
   const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[8]);
   const uint32_t acc_full0 = smem_u32(&bars[16]), acc_empty0 = smem_u32(&bars[18]);
 
@@ -1047,8 +1297,8 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         // keys cached by earlier passes for this CTA's first attention unit of
         // the layer: requested now, consumed after the next barrier
         int un = 0;
-        const AttnUnit U0 = attn_unit_from(P, rows, n0, c, G, un);
-        if (U0.valid) attn_issue(P, layer, U0, n0, A, 0, 0, tid);
+        const AttnUnit U0 = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, c, G, un);
+        if (U0.valid) attn_issue<kWide>(P, layer, U0, n0, A, 0, 0, tid);
         if (U0.valid || rstd_pending) cp_async_commit();  // (the staged partials are the group before)
       }
       auto ensure_rstd = [&]() {
@@ -1091,18 +1341,64 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             }
           }
         }
-      } else if (kind == PH_ATTN) {
-        // double-buffered units; the current unit's cached keys were requested in the QKV phase
+      } else if (kind == PH_ATTN && kWide) {
+        // units (kv head, page, 16-row block), double-buffered K/V; the first
+        // unit's cached keys were requested in the QKV phase
         int un = 0, un2 = 0;
-        AttnUnit cur = attn_unit_from(P, rows, n0, c, G, un);
+        AttnUnit cur = attn_unit_from<kAttnRowsW>(P, rows, n0, c, G, un);
         AttnUnit nxt{0, 0, 0, 0, false};
         if (cur.valid) {
-          attn_issue(P, layer, cur, n0, A, 0, 1, tid);
+          attn_issue<kWide>(P, layer, cur, n0, A, 0, 1, tid);
           cp_async_commit();
-          nxt = attn_unit_from(P, rows, n0, un, G, un2);
+          nxt = attn_unit_from<kAttnRowsW>(P, rows, n0, un, G, un2);
           if (nxt.valid) {
-            attn_issue(P, layer, nxt, n0, A, 1, 0, tid);
-            attn_issue(P, layer, nxt, n0, A, 1, 1, tid);
+            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 0, tid);
+            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 1, tid);
+          }
+          cp_async_commit();
+        }
+        for (int i = 0; cur.valid; ++i) {
+          cp_async_wait<1>();
+          wk_bar();
+          if (tid == 0 && i == 0) stamp(P, p, c, G, 7);
+          attention_unit_wide(P, cur, n0, A, i & 1, w, lane);
+          wk_bar();  // buffer i&1 is free again
+          if (tid == 0 && i == 0) stamp(P, p, c, G, 9);
+          AttnUnit nn{0, 0, 0, 0, false};
+          int un3 = un2;
+          if (nxt.valid) nn = attn_unit_from<kAttnRowsW>(P, rows, n0, un2, G, un3);
+          if (nn.valid) {
+            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 0, tid);
+            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 1, tid);
+          }
+          cp_async_commit();
+          cur = nxt;
+          nxt = nn;
+          un2 = un3;
+        }
+        // every page of every (row, head) is written: grid-wide sync on a
+        // second counter, then the merges spread over all warps of the grid
+        if (tid == 0) {
+          stamp(P, p, c, G, 10);
+          grid_arrive(P.bar2);
+          grid_wait(P.bar2, unsigned(G) * unsigned(layer + 1));
+        }
+        wk_bar();
+        const int items = rows * P.heads;
+        for (int it = c * 4 + w; it < items; it += 4 * G) attn_merge_one(P, n0, it / P.heads, it % P.heads, lane);
+        if (tid == 0) stamp(P, p, c, G, 11);
+      } else if (kind == PH_ATTN) {
+        // double-buffered units; the current unit's cached keys were requested in the QKV phase
+        int un = 0, un2 = 0, nlist = 0;
+        AttnUnit cur = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, c, G, un);
+        AttnUnit nxt{0, 0, 0, 0, false};
+        if (cur.valid) {
+          attn_issue<kWide>(P, layer, cur, n0, A, 0, 1, tid);
+          cp_async_commit();
+          nxt = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, un, G, un2);
+          if (nxt.valid) {
+            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 0, tid);
+            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 1, tid);
           }
           cp_async_commit();
         }
@@ -1110,18 +1406,35 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           cp_async_wait<1>();  // every group but the newest: the current unit's operands
           wk_bar();
           if (tid == 0 && i == 0) stamp(P, p, c, G, 7);
-          attention_unit(P, cur, n0, A, i & 1, w, lane, es.rflag, i == 0 ? p : -1);  // ends with wk_bar
+          attention_unit(P, cur, n0, A, i & 1, w, lane, i == 0 ? p : -1);  // ends with wk_bar
+          if (tid == 0) {
+            es.ulist[nlist][0] = cur.t0;
+            es.ulist[nlist][1] = cur.t1;
+            es.ulist[nlist][2] = cur.kvh;
+            es.ulist[nlist][3] = cur.s;
+          }
+          if (++nlist == 1) {  // decode: about one unit per CTA, count and merge right away
+            wk_bar();
+            attn_count_merge(P, n0, nlist, w, lane, es);  // ends with wk_bar
+            nlist = 0;
+          }
           AttnUnit nn{0, 0, 0, 0, false};
           int un3 = un2;
-          if (nxt.valid) nn = attn_unit_from(P, rows, n0, un2, G, un3);
+          if (nxt.valid) nn = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, un2, G, un3);
           if (nn.valid) {  // into the buffer just consumed
-            attn_issue(P, layer, nn, n0, A, i & 1, 0, tid);
-            attn_issue(P, layer, nn, n0, A, i & 1, 1, tid);
+            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 0, tid);
+            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 1, tid);
           }
           cp_async_commit();
           cur = nxt;
           nxt = nn;
           un2 = un3;
+        }
+        if (nlist > 0) {
+          wk_bar();
+          if (tid == 0) stamp(P, p, c, G, 10);
+          attn_count_merge(P, n0, nlist, w, lane, es);
+          if (tid == 0) stamp(P, p, c, G, 11);
         }
       } else {
         if (P.lm_only) {  // LM head over resident rows: the final rstd of each position is cached

@@ -207,7 +207,7 @@ struct ps_handle {
   std::vector<int> xmaps_ready;             // per ntok/16
   __nv_bfloat16* qkv_bias_all = nullptr;
   float* mega_part = nullptr;
-  unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [64..] per-phase tile counters
+  unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [2]=bar2, [64..] per-phase tile counters
   int mega_max_tiles = 0;
   size_t mega_cnt_words = 0;
   unsigned* mega_epoch = nullptr;
@@ -409,7 +409,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   using bf = __nv_bfloat16;
   const int ntok = round_up(std::max(max_rows, 1), 16);
   const int grp = h->nh / h->nkv;
-  const int attn_floats = mega_attn_bytes(h->hd, grp) / 4;
+  const int attn_floats = mega_attn_bytes(h->hd, grp, max_rows > 1, h->H) / 4;
   MegaParams P{};
   P.ctx = ctx;
   P.decode = decode ? 1 : 0;
@@ -460,6 +460,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.am_idx = h->am_idx;
   P.keys = (sharded && !lm_only) ? h->keys : nullptr;
   P.bar = h->mega_cnt;
+  P.bar2 = h->mega_cnt + 2;
   P.lm_only = lm_only ? 1 : 0;
   P.logits_out = logits_out;
   P.ld_logits = h->v_count;
@@ -884,12 +885,13 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     cudaMemcpy(h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
     // every pass width must fit one CTA per SM (co-residency of the grid)
     const int grp = h->nh / h->nkv;
-    const int attn_floats = mega_attn_bytes(h->hd, grp) / 4;
-    for (int ntok = 16; ntok <= kMaxWindow; ntok += 16) {
-      const int st = mega_stages(ntok, attn_floats);
-      if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats)) < 1)
-        return (ps_destroy(h), fail(PS_ERR_CUDA, "megakernel does not fit one CTA per SM"));
-    }
+    for (int ntok = 16; ntok <= kMaxWindow; ntok += 16)
+      for (int wide = 0; wide < 2; ++wide) {
+        const int attn_floats = mega_attn_bytes(h->hd, grp, wide != 0, h->H) / 4;
+        const int st = mega_stages(ntok, attn_floats);
+        if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats)) < 1)
+          return (ps_destroy(h), fail(PS_ERR_CUDA, "megakernel does not fit one CTA per SM"));
+      }
   }
   {
     // RoPE table (rotate-half pairs): angle = pos * theta^(-2i/hd), in fp64.
