@@ -1543,10 +1543,27 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         if constexpr (kWide) {
           // second pass: wait for the split tiles' pieces, then finalise this
           // CTA's row share of each (every piece's CTA takes a share)
+          // Row shares are weighted so that every CTA finalises about the same
+          // number of rows in total: a CTA with two split tiles (its first and
+          // last piece) takes half-weight shares of each.
+          auto split_pieces = [&](int cc) {
+            const int lo = sk_start(cc, g.G, g.T), hi = sk_start(cc + 1, g.G, g.T);
+            const int t0 = lo / g.KB, t1 = (hi - 1) / g.KB;
+            const int first = (lo != t0 * g.KB || hi < (t0 + 1) * g.KB) ? 1 : 0;
+            const int last = (t1 != t0 && hi != (t1 + 1) * g.KB) ? 1 : 0;
+            return first + last;
+          };
           auto def_of = [&](int tile) {
             const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
-            const int npieces = c_last - c_first + 1, my_idx = c - c_first;
-            return DefTile{tile, c_first, npieces, my_idx * rows / npieces, (my_idx + 1) * rows / npieces,
+            const int npieces = c_last - c_first + 1;
+            int wsum = 0, wbefore = 0, wmine = 0;
+            for (int pc = 0; pc < npieces; ++pc) {
+              const int wt = split_pieces(c_first + pc) > 1 ? 1 : 2;
+              if (c_first + pc < c) wbefore += wt;
+              if (c_first + pc == c) wmine = wt;
+              wsum += wt;
+            }
+            return DefTile{tile, c_first, npieces, wbefore * rows / wsum, (wbefore + wmine) * rows / wsum,
                            first_piece_slot(c_first, tile, g)};
           };
           // dtile1 is only set once dtile0 is
