@@ -143,6 +143,21 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// The finishing arithmetic of every GEMM epilogue, spelled with explicit
+// rounding so that the TMEM-lane epilogues (finish_chunk) and the vectorised
+// wide-pass finalisation (finish_share_vec) compute bitwise the same values.
+__device__ __forceinline__ float epi_scale_bias(float acc, float rstd, float bias) { return fmaf(acc, rstd, bias); }
+// RoPE on a rotate-half pair: the even row holds dim i, the odd row dim i+hd/2
+__device__ __forceinline__ float rope_even(float val, float other, float c, float s) {
+  return fmaf(val, c, -__fmul_rn(other, s));
+}
+__device__ __forceinline__ float rope_odd(float val, float other, float c, float s) {
+  return fmaf(val, c, __fmul_rn(other, s));
+}
+__device__ __forceinline__ float swiglu(float gate, float up) {
+  return __fmul_rn(__fdividef(gate, __fadd_rn(1.0f, ex2(__fmul_rn(gate, -1.4426950408889634f)))), up);
+}
+
 // ---------------------------------------------------------------------------
 // epilogue math for one finished 8-column chunk of tile rows [128*tile, +128)
 struct EpiSmem {
@@ -154,6 +169,7 @@ struct EpiSmem {
   int flag;
   int rflag[32 * 4];  // [unit][row] of the ATT phase's deferred unit list
   int ulist[32][4];   // (t0, t1, kv head, page) of units computed, not yet counted
+  int pg[8];          // wide passes: physical KV pages of logical pages n0/64 .. (n0+rows-1)/64
 };
 
 // Barrier-free: every warp finishes its own 32 rows. RoPE / SwiGLU partners
@@ -213,12 +229,12 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
     for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
       const bool valid = t < rows;
-      const float val = valid ? v[j] * es.rstd[t] + bias : 0.f;
+      const float val = valid ? epi_scale_bias(v[j], es.rstd[t], bias) : 0.f;
       const float other = __shfl_xor_sync(0xffffffffu, val, 1);
       if (!valid) continue;
       const int pos = n0 + t;
       float out = val;
-      if (is_q || is_k) out = even ? val * cs[j].x - other * cs[j].y : val * cs[j].x + other * cs[j].y;
+      if (is_q || is_k) out = even ? rope_even(val, other, cs[j].x, cs[j].y) : rope_odd(val, other, cs[j].x, cs[j].y);
       const __nv_bfloat16 ob = __float2bfloat16_rn(out);
       const int col = n - r + dim;  // original (unpermuted) output column
       if (is_q) {
@@ -235,10 +251,9 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const int t = c0 + j;
-      const float val = t < rows ? v[j] * es.rstd[t] : 0.f;
+      const float val = t < rows ? __fmul_rn(v[j], es.rstd[t]) : 0.f;
       const float up = __shfl_xor_sync(0xffffffffu, val, 1);
-      if (t < rows && (m & 1) == 0)
-        P.act[size_t(t) * P.I + tile * 64 + (m >> 1)] = __float2bfloat16_rn(__fdividef(val, 1.0f + ex2(val * -1.4426950408889634f)) * up);
+      if (t < rows && (m & 1) == 0) P.act[size_t(t) * P.I + tile * 64 + (m >> 1)] = __float2bfloat16_rn(swiglu(val, up));
     }
   } else if (kind == PH_O || kind == PH_D) {
     const bool to_hn = kind == PH_D && layer == P.L - 1;
@@ -250,11 +265,11 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       sq[j] = 0.f;
       if (t < rows) {
         float* xp = P.x + size_t(t) * P.H + n;
-        const float xi = xo[j] + v[j];
+        const float xi = __fadd_rn(xo[j], v[j]);
         *xp = xi;
         __nv_bfloat16* dst = to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H;
         dst[n] = __float2bfloat16_rn(xi);
-        sq[j] = xi * xi;
+        sq[j] = __fmul_rn(xi, xi);
       }
     }
     if constexpr (NR == 8) {
@@ -297,7 +312,7 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
       lv[j] = -INFINITY;
       li[j] = 0x7fffffff;
       if (valid && t < rows) {
-        lv[j] = v[j] * es.rstd[t] + b;
+        lv[j] = epi_scale_bias(v[j], es.rstd[t], b);
         li[j] = vid;
         if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n] = lv[j];  // exactly the values the argmax sees
       }
@@ -1071,6 +1086,138 @@ struct DefTile {
   int tile, c_first, npieces, r_lo, r_hi, slot0;
 };
 
+// Wide passes: a split tile's row share, finalised from shared memory with a
+// vectorised thread map. The pieces' partial rows (contiguous per piece slot)
+// and the per-row inputs (residual rows for O/D, RoPE rows for QKV) are
+// fetched with 1D bulk copies by one thread onto an mbarrier; then thread
+// (fg, w) handles features 4fg..4fg+3 of rows r_lo+w, r_lo+w+4, ... RoPE and
+// SwiGLU partners are in-thread; the O/D row sums of squares follow warp_sum's
+// pairing (feature bits 4,3,2 across lanes, then 1,0 in-thread), so every value
+// is bitwise the TMEM-lane epilogue's (finish_chunk / finish_tagged).
+__device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, int layer, int n0, int w, int lane,
+                                                 const DefTile& T, float* S, int cap_floats, uint32_t wbar,
+                                                 uint32_t& wphase, EpiSmem& es) {
+  const int tid = threadIdx.x - 64;
+  const int np = T.npieces;
+  const bool has_x = kind == PH_O || kind == PH_D;
+  const bool has_rope = kind == PH_QKV;
+  const int hd = P.hd, half = hd >> 1;
+  const int rope_row = half * 2;  // floats per RoPE row (cos, sin pairs)
+  const int per_row = np * 128 + (has_x ? 128 : has_rope ? rope_row : 0);
+  const int batch = cap_floats / per_row;  // >= 8 rows
+  const int f0 = 4 * lane;               // this thread's first feature within the tile
+  const int n = T.tile * 128 + f0;
+  for (int b0 = T.r_lo; b0 < T.r_hi; b0 += batch) {
+    const int nb = min(batch, T.r_hi - b0);
+    float* X = S + np * nb * 128;
+    if (tid == 0) {
+      fence_proxy_async_global();  // generic writes of other CTAs (acquired) -> async-proxy reads
+      const uint32_t bytes = uint32_t(np * nb * 512 + (has_x ? nb * 512 : has_rope ? nb * rope_row * 4 : 0));
+      mbar_expect_tx(wbar, bytes);
+      for (int pc = 0; pc < np; ++pc)
+        bulk_g2s(smem_u32(S + pc * nb * 128),
+                 P.part + piece_off_slot(T.c_first + pc, pc == 0 ? T.slot0 : 0, 0) + size_t(b0) * 128, nb * 512, wbar);
+      if (has_x)
+        for (int r = 0; r < nb; ++r) bulk_g2s(smem_u32(X + r * 128), P.x + size_t(b0 + r) * P.H + T.tile * 128, 512, wbar);
+      else if (has_rope)
+        bulk_g2s(smem_u32(X), P.rope + size_t(n0 + b0) * half, uint32_t(nb * rope_row * 4), wbar);
+    }
+    mbar_wait(wbar, wphase);
+    wphase ^= 1u;
+    for (int r = w; r < nb; r += 4) {
+      const int t = b0 + r;
+      float4 acc = *reinterpret_cast<const float4*>(S + r * 128 + f0);
+      for (int pc = 1; pc < np; ++pc) {
+        const float4 o = *reinterpret_cast<const float4*>(S + (pc * nb + r) * 128 + f0);
+        acc.x += o.x;
+        acc.y += o.y;
+        acc.z += o.z;
+        acc.w += o.w;
+      }
+      if (kind == PH_QKV) {
+        const int rr = n & (hd - 1), pi0 = rr >> 1;  // features f0, f0+1 = dims pi0, pi0+half; f0+2, f0+3 = pi0+1, ..
+        const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
+        float bias[4] = {0.f, 0.f, 0.f, 0.f};
+        if (P.qkv_bias) {
+          const __nv_bfloat16* bp = P.qkv_bias + size_t(layer) * (P.qd + 2 * P.kvd) + n;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) bias[e] = __bfloat162float(bp[e]);
+        }
+        const float rs = es.rstd[t];
+        const float v0 = epi_scale_bias(acc.x, rs, bias[0]), v1 = epi_scale_bias(acc.y, rs, bias[1]);
+        const float v2 = epi_scale_bias(acc.z, rs, bias[2]), v3 = epi_scale_bias(acc.w, rs, bias[3]);
+        float o0 = v0, o1 = v1, o2 = v2, o3 = v3;
+        if (is_q || is_k) {
+          const float4 cs = *reinterpret_cast<const float4*>(X + r * rope_row + 2 * pi0);  // (c, s) of pi0, pi0+1
+          o0 = rope_even(v0, v1, cs.x, cs.y);
+          o1 = rope_odd(v1, v0, cs.x, cs.y);
+          o2 = rope_even(v2, v3, cs.z, cs.w);
+          o3 = rope_odd(v3, v2, cs.z, cs.w);
+        }
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(o0, o2), hi = __floats2bfloat162_rn(o1, o3);
+        const int col = n - rr + pi0;  // original column of dim pi0 (the odd rows are dims + half)
+        __nv_bfloat16* d;
+        if (is_q) {
+          d = P.q + size_t(t) * P.qd + col;
+        } else {
+          const int pos = n0 + t;
+          const int cc = col - P.qd - (is_k ? 0 : P.kvd);
+          const int h = cc >> P.hd_shift;
+          const int page = es.pg[(pos >> 6) - (n0 >> 6)];
+          d = (is_k ? P.kpool : P.vpool) + size_t(layer) * P.g.layer_stride() +
+              ((size_t(page) * P.g.kv_heads + h) * kPage + (pos & (kPage - 1))) * hd + (cc & (hd - 1));
+        }
+        *reinterpret_cast<__nv_bfloat162*>(d) = lo;
+        *reinterpret_cast<__nv_bfloat162*>(d + half) = hi;
+      } else if (kind == PH_GU) {
+        const float rs = es.rstd[t];
+        const float g0 = __fmul_rn(acc.x, rs), u0 = __fmul_rn(acc.y, rs);
+        const float g1 = __fmul_rn(acc.z, rs), u1 = __fmul_rn(acc.w, rs);
+        *reinterpret_cast<__nv_bfloat162*>(P.act + size_t(t) * P.I + T.tile * 64 + 2 * lane) =
+            __floats2bfloat162_rn(swiglu(g0, u0), swiglu(g1, u1));
+      } else if (kind == PH_O || kind == PH_D) {
+        const float4 xo = *reinterpret_cast<const float4*>(X + r * 128 + f0);
+        const float4 xi = make_float4(__fadd_rn(xo.x, acc.x), __fadd_rn(xo.y, acc.y), __fadd_rn(xo.z, acc.z),
+                                      __fadd_rn(xo.w, acc.w));
+        *reinterpret_cast<float4*>(P.x + size_t(t) * P.H + n) = xi;
+        const bool to_hn = kind == PH_D && layer == P.L - 1;
+        __nv_bfloat16* dst = (to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H) + n;
+        const __nv_bfloat162 b01 = __floats2bfloat162_rn(xi.x, xi.y), b23 = __floats2bfloat162_rn(xi.z, xi.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&b01);
+        pk.y = *reinterpret_cast<const uint32_t*>(&b23);
+        *reinterpret_cast<uint2*>(dst) = pk;
+        float s0 = __fmul_rn(xi.x, xi.x), s1 = __fmul_rn(xi.y, xi.y), s2 = __fmul_rn(xi.z, xi.z), s3 = __fmul_rn(xi.w, xi.w);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+          s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+        }
+        const float tot = (s0 + s2) + (s1 + s3);
+        if ((lane & 7) == 0) P.ssq_part[size_t(T.tile * 4 + (lane >> 3)) * kMaxWindow + t] = tot;
+      } else {  // PH_LM
+        const float rs = es.rstd[t];
+        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+        float bv = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (n + e < P.vocab_local) {
+            const float lv = epi_scale_bias(a4[e], rs, P.lm_bias[P.v_begin + n + e]);
+            if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n + e] = lv;
+            argmax_merge(bv, bi, lv, P.v_begin + n + e);
+          }
+        }
+        warp_argmax(bv, bi);
+        if (lane == 0) argmax_merge(es.am_v[w][t], es.am_i[w][t], bv, bi);
+      }
+    }
+    wk_bar();  // the staging area is reused by the next batch / tile
+  }
+}
+
 }  // namespace
 
 // kWide: passes of more than one row (verify / prefill chunks / Jacobi
@@ -1082,7 +1229,7 @@ struct DefTile {
 template <bool kWide>
 __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ MegaParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ uint64_t bars[2 * 8 + 4];
+  __shared__ uint64_t bars[2 * 8 + 4 + 1];
   __shared__ uint32_t tmem_holder;
   __shared__ EpiSmem es;
 
@@ -1109,6 +1256,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       mbar_init(acc_full0 + 8 * b, 1);
       mbar_init(acc_empty0 + 8 * b, 1);
     }
+    mbar_init(smem_u32(&bars[20]), 1);  // workers' bulk staging (wide finalisation)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -1234,6 +1382,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
     const int m = q * 32 + lane;  // row within a 128-row tile
     const int tid = threadIdx.x - 64;
     uint32_t acc_it = 0;
+    uint32_t wphase = 0;  // parity of the workers' staging mbarrier
+    if (kWide && tid < 8) {
+      const int lp = (n0 >> 6) + tid;
+      es.pg[tid] = lp <= ((n0 + rows - 1) >> 6) ? P.page_table[lp] : 0;
+    }
     // ---- phase 0: embedding rows (t ≡ c mod G) ----
     for (int t = c; t < (P.lm_only ? 0 : rows); t += G) {
       const int pos = n0 + t;
@@ -1577,11 +1730,14 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           }
           wk_bar();
           if (tid == 0) stamp(P, p, c, G, 8);
+          // staging area: both attention buffers, except in QKV where buffer 0
+          // holds the next ATTN phase's prefetched keys
+          float* stage = reinterpret_cast<float*>(kind == PH_QKV ? A.K(1) : A.K(0));
+          const int cap = (kind == PH_QKV ? A.buf : 2 * A.buf) / 4;
 #pragma unroll
           for (int d = 0; d < 2; ++d)
             if (d < nd && D[d].r_lo < D[d].r_hi)
-              finish_from_pieces(P, kind, layer, D[d].r_lo, D[d].r_hi, n0, D[d].tile, m, q, lane, D[d].c_first,
-                                 D[d].npieces, g, es, d == 0 ? p : -1);
+              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, smem_u32(&bars[20]), wphase, es);
           if (tid == 0) stamp(P, p, c, G, 9);
         }
         if (tid == 0) stamp(P, p, c, G, 6);
