@@ -487,7 +487,9 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
     P.pre_max = max_rows > 1 ? pre_wide : pre_dec;
     for (int k = 0; k < 5; ++k) P.pf[1 + (k == 0 ? 0 : k + 1)] = pf[k];  // kinds QKV=1, O=3, GU=4, D=5, LM=6
   }
-  cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned) * h->mega_cnt_words, h->st);
+  // 1-row passes use only the barrier words (the per-phase tile counters
+  // serve the wide finalisation)
+  cudaMemsetAsync(h->mega_cnt, 0, sizeof(unsigned) * (max_rows > 1 ? h->mega_cnt_words : 64), h->st);
   prof_mark(h, 7);
   const cudaError_t e = launch_mega(P, max_rows > 1, h->sms, mega_smem_bytes(ntok, P.stages, attn_floats), h->st);
   if (e != cudaSuccess) std::fprintf(stderr, "predgen_b200: megakernel launch failed: %s\n", cudaGetErrorString(e));
