@@ -166,8 +166,8 @@ struct MegaParams {
   int pre_max;              // weight stages issued ahead of a phase barrier (<= stages)
   int pf[8];                // per phase kind: weight boxes L2-prefetched ahead of the phase barrier
 };
-// attention staging of the megakernel (see AttnSmem in megakernel.cu): two
-// unit buffers of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
+// attention staging of the megakernel (see AttnSmem in megakernel.cu): decode
+// passes one unit buffer of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
 // wide passes: K and V only (q fragments are read from global memory); a
 // buffer also holds the staged RMSNorm partials of up to kRstdStageRows rows
 constexpr int kRstdStageRows = 80;
@@ -176,7 +176,7 @@ __host__ __device__ inline int mega_attn_buf_wide(int hd, int H) {
   return kv > rs ? kv : rs;
 }
 inline int mega_attn_bytes(int hd, int grp, bool wide, int H) {
-  return wide ? 2 * mega_attn_buf_wide(hd, H) : 2 * (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2);
+  return wide ? 2 * mega_attn_buf_wide(hd, H) : (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2);
 }
 int mega_stages(int ntok, int attn_floats);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);

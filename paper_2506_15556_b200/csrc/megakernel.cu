@@ -1229,7 +1229,8 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
 template <bool kWide>
 __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ MegaParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ uint64_t bars[2 * 8 + 4 + 1];
+  // [full x kMaxStages][empty x kMaxStages][acc_full x 2][acc_empty x 2][workers' staging]
+  __shared__ uint64_t bars[2 * kMaxStages + 4 + 1];
   __shared__ uint32_t tmem_holder;
   __shared__ EpiSmem es;
 
@@ -1244,8 +1245,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   auto a_tile = [&](int s) { return base + size_t(s) * (kTileABytes + b_bytes); };
   auto b_tile = [&](int s) { return a_tile(s) + kTileABytes; };
   const AttnSmem A = attn_smem(base + size_t(ST) * (kTileABytes + b_bytes), P.hd, P.heads / P.kv_heads, kWide, P.H);
-  const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[8]);
-  const uint32_t acc_full0 = smem_u32(&bars[16]), acc_empty0 = smem_u32(&bars[18]);
+  const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[kMaxStages]);
+  const uint32_t acc_full0 = smem_u32(&bars[2 * kMaxStages]), acc_empty0 = smem_u32(&bars[2 * kMaxStages + 2]);
+  const uint32_t wbar = smem_u32(&bars[2 * kMaxStages + 4]);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -1256,7 +1258,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       mbar_init(acc_full0 + 8 * b, 1);
       mbar_init(acc_empty0 + 8 * b, 1);
     }
-    mbar_init(smem_u32(&bars[20]), 1);  // workers' bulk staging (wide finalisation)
+    mbar_init(wbar, 1);  // workers' bulk staging (wide finalisation)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -1541,53 +1543,30 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         for (int it = c * 4 + w; it < items; it += 4 * G) attn_merge_one(P, n0, it / P.heads, it % P.heads, lane);
         if (tid == 0) stamp(P, p, c, G, 11);
       } else if (kind == PH_ATTN) {
-        // double-buffered units; the current unit's cached keys were requested in the QKV phase
-        int un = 0, un2 = 0, nlist = 0;
-        AttnUnit cur = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, c, G, un);
-        AttnUnit nxt{0, 0, 0, 0, false};
-        if (cur.valid) {
+        // decode: about one unit per CTA, so one operand buffer (the smem it
+        // frees deepens the weight ring); the first unit's cached keys were
+        // requested in the QKV phase
+        int un = 0;
+        AttnUnit cur = attn_unit_from<kAttnRows>(P, rows, n0, c, G, un);
+        for (int i = 0; cur.valid; ++i) {
+          if (i > 0) attn_issue<kWide>(P, layer, cur, n0, A, 0, 0, tid);
           attn_issue<kWide>(P, layer, cur, n0, A, 0, 1, tid);
           cp_async_commit();
-          nxt = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, un, G, un2);
-          if (nxt.valid) {
-            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 0, tid);
-            attn_issue<kWide>(P, layer, nxt, n0, A, 1, 1, tid);
-          }
-          cp_async_commit();
-        }
-        for (int i = 0; cur.valid; ++i) {
-          cp_async_wait<1>();  // every group but the newest: the current unit's operands
+          cp_async_wait<0>();
           wk_bar();
           if (tid == 0 && i == 0) stamp(P, p, c, G, 7);
-          attention_unit(P, cur, n0, A, i & 1, w, lane, i == 0 ? p : -1);  // ends with wk_bar
+          attention_unit(P, cur, n0, A, 0, w, lane, i == 0 ? p : -1);  // ends with wk_bar
           if (tid == 0) {
-            es.ulist[nlist][0] = cur.t0;
-            es.ulist[nlist][1] = cur.t1;
-            es.ulist[nlist][2] = cur.kvh;
-            es.ulist[nlist][3] = cur.s;
+            es.ulist[0][0] = cur.t0;
+            es.ulist[0][1] = cur.t1;
+            es.ulist[0][2] = cur.kvh;
+            es.ulist[0][3] = cur.s;
           }
-          if (++nlist == 1) {  // decode: about one unit per CTA, count and merge right away
-            wk_bar();
-            attn_count_merge(P, n0, nlist, w, lane, es);  // ends with wk_bar
-            nlist = 0;
-          }
-          AttnUnit nn{0, 0, 0, 0, false};
-          int un3 = un2;
-          if (nxt.valid) nn = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, un2, G, un3);
-          if (nn.valid) {  // into the buffer just consumed
-            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 0, tid);
-            attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 1, tid);
-          }
-          cp_async_commit();
-          cur = nxt;
-          nxt = nn;
-          un2 = un3;
-        }
-        if (nlist > 0) {
           wk_bar();
-          if (tid == 0) stamp(P, p, c, G, 10);
-          attn_count_merge(P, n0, nlist, w, lane, es);
-          if (tid == 0) stamp(P, p, c, G, 11);
+          attn_count_merge(P, n0, 1, w, lane, es);  // ends with wk_bar
+          int un2 = un;
+          cur = attn_unit_from<kAttnRows>(P, rows, n0, un, G, un2);
+          un = un2;
         }
       } else {
         if (P.lm_only) {  // LM head over resident rows: the final rstd of each position is cached
@@ -1737,7 +1716,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
 #pragma unroll
           for (int d = 0; d < 2; ++d)
             if (d < nd && D[d].r_lo < D[d].r_hi)
-              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, smem_u32(&bars[20]), wphase, es);
+              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, wbar, wphase, es);
           if (tid == 0) stamp(P, p, c, G, 9);
         }
         if (tid == 0) stamp(P, p, c, G, 6);
@@ -1802,7 +1781,7 @@ int mega_stages(int ntok, int attn_floats) {
   // 1 KB alignment slack
   const int avail = 227 * 1024 - static_smem - attn_floats * 4 - 1024;
   int s = avail / stage;
-  return s > 8 ? 8 : s;
+  return s > kMaxStages ? kMaxStages : s;
 }
 
 int mega_smem_bytes(int ntok, int stages, int attn_floats) {

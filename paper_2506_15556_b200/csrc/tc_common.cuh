@@ -9,6 +9,7 @@
 namespace ps {
 
 constexpr int kBK = 64;                         // K elements per stage (128 B rows)
+constexpr int kMaxStages = 12;                  // weight ring depth limit (smem decides the actual depth)
 constexpr int kTileABytes = 128 * kBK * 2;      // 16 KB weight tile (M = 128)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
