@@ -178,10 +178,10 @@ __host__ __device__ inline int mega_attn_buf_wide(int hd, int H) {
 inline int mega_attn_bytes(int hd, int grp, bool wide, int H) {
   return wide ? 2 * mega_attn_buf_wide(hd, H) : (2 * kPage * (hd + 8) * 2 + 4 * grp * (hd + 8) * 2);
 }
-int mega_stages(int ntok, int attn_floats);
+int mega_stages(int ntok, int attn_floats, bool wide);
 int mega_smem_bytes(int ntok, int stages, int attn_floats);
 // wide: the pass may have more than one row (max_rows > 1)
 cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cudaStream_t st);
-int mega_max_blocks_per_sm(int smem);
+int mega_max_blocks_per_sm(int smem, bool wide);
 
 }  // namespace ps

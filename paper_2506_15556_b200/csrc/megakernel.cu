@@ -160,12 +160,15 @@ __device__ __forceinline__ float swiglu(float gate, float up) {
 
 // ---------------------------------------------------------------------------
 // epilogue math for one finished 8-column chunk of tile rows [128*tile, +128)
-struct EpiSmem {
-  float am_v[4][kMaxWindow];  // LM head: running (max, id) per warp quadrant and row
-  int am_i[4][kMaxWindow];
+// RW: rows a pass of this instantiation can have (decode: 1, sized 16)
+template <int RW>
+struct EpiSmemT {
+  static constexpr int kRows = RW;
+  float am_v[4][RW];  // LM head: running (max, id) per warp quadrant and row
+  int am_i[4][RW];
   float red_v[4][8];
   int red_i[4][8];
-  float rstd[kMaxWindow];
+  float rstd[RW];
   int flag;
   int rflag[32 * 4];  // [unit][row] of the ATT phase's deferred unit list
   int ulist[32][4];   // (t0, t1, kv head, page) of units computed, not yet counted
@@ -207,9 +210,9 @@ __device__ __forceinline__ void epi_load(const MegaParams& P, int kind, int rows
   }
 }
 
-template <int NR = 8>
+template <int NR = 8, class ES>
 __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int layer, int rows, int n0, int tile, int m, int q,
-                             int lane, int c0, const float (&v)[8], EpiSmem& es, const EpiPre& pre) {
+                             int lane, int c0, const float (&v)[8], ES& es, const EpiPre& pre) {
   const int n = tile * 128 + m;
   if (kind == PH_QKV) {
     const int hd = P.hd, half = hd >> 1;
@@ -360,7 +363,8 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
 // pass has up to 256 rows; one L2 round trip per row was the verify pass's
 // largest worker cost).
 constexpr int kRstdBatch = 4;
-__device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, EpiSmem& es) {
+template <class ES>
+__device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, ES& es) {
   if (from_embed) {
     for (int t = w * 32 + lane; t < rows; t += kWorkers) es.rstd[t] = __ldcg(P.rstd0 + t);
     return;
@@ -455,8 +459,9 @@ __device__ __forceinline__ void rstd_stage_issue(const MegaParams& P, const Attn
   for (int e = w; e < nparts; e += 4)
     for (int v = 4 * lane; v < ld; v += 128) cp_async16(S + e * ld + v, P.ssq_part + size_t(e) * kMaxWindow + v);
 }
+template <class ES>
 __device__ __forceinline__ void rstd_stage_reduce(const MegaParams& P, const AttnSmem& A, int rows, int w, int lane,
-                                                  EpiSmem& es) {
+                                                  ES& es) {
   const float* S = reinterpret_cast<const float*>(A.K(1));
   const int nparts = 4 * (P.H / 128), ld = rstd_stage_ld(rows);
   for (int g0 = w * 8; g0 < rows; g0 += 32) {
@@ -957,7 +962,8 @@ __device__ __forceinline__ void attn_merge_one(const MegaParams& P, int n0, int 
 // the last page of a (row, kv head) merges its grp heads, one warp per (row,
 // head): lane sp owns page sp for the scalars (fixed butterfly); the output
 // sums run over pages in order, loads batched.
-__device__ __forceinline__ void attn_count_merge(const MegaParams& P, int n0, int nunits, int w, int lane, EpiSmem& es) {
+template <class ES>
+__device__ __forceinline__ void attn_count_merge(const MegaParams& P, int n0, int nunits, int w, int lane, ES& es) {
   const int tid = threadIdx.x - 64;
   const int hd = P.hd, grp = P.heads / P.kv_heads;
   if (tid < nunits * kAttnRows) {
@@ -1018,9 +1024,10 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
 // c_first) plus the tagged partials of CTAs c_first+1 .. c_first+npieces-1,
 // summed in CTA order (the order of finish_from_pieces), then the phase's
 // finishing math. The O/D residual load is issued with the partial loads.
+template <class ES>
 __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int layer, int n0, int tile, int m, int q,
                                               int lane, int c_first, int npieces, const Gemm& g, unsigned tag, float own,
-                                              EpiSmem& es) {
+                                              ES& es) {
   const unsigned long long* part = reinterpret_cast<const unsigned long long*>(P.part);
   EpiPre pre;
   epi_load<1>(P, kind, 1, n0, tile, m, 0, pre);
@@ -1048,9 +1055,10 @@ __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int
 
 // Sum a split tile's piece partials (pieces = CTAs c_first.., in CTA order,
 // all loads in flight) for rows [r_lo, r_hi) and run the finishing math.
+template <class ES>
 __device__ __forceinline__ void finish_from_pieces(const MegaParams& P, int kind, int layer, int r_lo, int r_hi, int n0,
                                                    int tile, int m, int q, int lane, int c_first, int npieces,
-                                                   const Gemm& g, EpiSmem& es, int trace_p = -1) {
+                                                   const Gemm& g, ES& es, int trace_p = -1) {
   int off[8];
 #pragma unroll
   off[0] = piece_off_slot(c_first, first_piece_slot(c_first, tile, g), m);
@@ -1094,9 +1102,10 @@ struct DefTile {
 // SwiGLU partners are in-thread; the O/D row sums of squares follow warp_sum's
 // pairing (feature bits 4,3,2 across lanes, then 1,0 in-thread), so every value
 // is bitwise the TMEM-lane epilogue's (finish_chunk / finish_tagged).
+template <class ES>
 __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, int layer, int n0, int w, int lane,
                                                  const DefTile& T, float* S, int cap_floats, uint32_t wbar,
-                                                 uint32_t& wphase, EpiSmem& es) {
+                                                 uint32_t& wphase, ES& es) {
   const int tid = threadIdx.x - 64;
   const int np = T.npieces;
   const bool has_x = kind == PH_O || kind == PH_D;
@@ -1232,7 +1241,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   // [full x kMaxStages][empty x kMaxStages][acc_full x 2][acc_empty x 2][workers' staging]
   __shared__ uint64_t bars[2 * kMaxStages + 4 + 1];
   __shared__ uint32_t tmem_holder;
-  __shared__ EpiSmem es;
+  __shared__ EpiSmemT<kWide ? kMaxWindow : 16> es;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x, G = gridDim.x;
@@ -1589,9 +1598,10 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         constexpr bool spread = kWide;
         int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
         if (kind == PH_LM) {
-          for (int e = tid; e < 4 * kMaxWindow; e += kWorkers) {
-            es.am_v[e / kMaxWindow][e % kMaxWindow] = -INFINITY;
-            es.am_i[e / kMaxWindow][e % kMaxWindow] = 0x7fffffff;
+          constexpr int RW = decltype(es)::kRows;
+          for (int e = tid; e < 4 * RW; e += kWorkers) {
+            es.am_v[e / RW][e % RW] = -INFINITY;
+            es.am_i[e / RW][e % RW] = 0x7fffffff;
           }
           wk_bar();
         }
@@ -1749,33 +1759,33 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
   }
 }
 
-int mega_static_smem() {
-  static int static_smem = -1;
-  if (static_smem < 0) {
-    cudaFuncAttributes fa{}, fb{};
-    static_smem = cudaFuncGetAttributes(&fa, mega_kernel<false>) == cudaSuccess &&
-                          cudaFuncGetAttributes(&fb, mega_kernel<true>) == cudaSuccess
-                      ? int(fa.sharedSizeBytes > fb.sharedSizeBytes ? fa.sharedSizeBytes : fb.sharedSizeBytes)
-                      : 16 * 1024;
+// static shared memory of one instantiation (the decode kernel's EpiSmem is small)
+int mega_static_smem(bool wide) {
+  static int st[2] = {-1, -1};
+  if (st[wide] < 0) {
+    cudaFuncAttributes fa{};
+    const cudaError_t e = wide ? cudaFuncGetAttributes(&fa, mega_kernel<true>) : cudaFuncGetAttributes(&fa, mega_kernel<false>);
+    st[wide] = e == cudaSuccess ? int(fa.sharedSizeBytes) : 16 * 1024;
   }
-  return static_smem;
+  return st[wide];
 }
 
-// One fixed attribute (the most any pass width may use), set once, so
-// handles created later never shrink it under a running configuration.
+// One fixed attribute per instantiation (the most any pass width may use),
+// set once, so handles created later never shrink it under a running one.
 cudaError_t mega_set_smem_attr() {
   static cudaError_t done = cudaErrorNotReady;
   if (done == cudaErrorNotReady) {
-    const int bytes = 227 * 1024 - mega_static_smem();
-    done = cudaFuncSetAttribute(mega_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done = cudaFuncSetAttribute(mega_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024 - mega_static_smem(false));
     if (done == cudaSuccess)
-      done = cudaFuncSetAttribute(mega_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      done = cudaFuncSetAttribute(mega_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024 - mega_static_smem(true));
   }
   return done;
 }
 
-int mega_stages(int ntok, int attn_floats) {
-  const int static_smem = mega_static_smem();
+int mega_stages(int ntok, int attn_floats, bool wide) {
+  const int static_smem = mega_static_smem(wide);
   const int stage = kTileABytes + ntok * 128;
   // 227 KB per CTA minus static shared memory, attention staging and the
   // 1 KB alignment slack
@@ -1803,14 +1813,12 @@ cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cuda
   return wide ? cudaLaunchKernelEx(&cfg, mega_kernel<true>, P) : cudaLaunchKernelEx(&cfg, mega_kernel<false>, P);
 }
 
-int mega_max_blocks_per_sm(int smem) {
+int mega_max_blocks_per_sm(int smem, bool wide) {
   if (mega_set_smem_attr() != cudaSuccess) return 0;
   int n = 0;
-  int n2 = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<false>, 192, smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, mega_kernel<true>, 192, smem) != cudaSuccess)
-    return 0;
-  return n < n2 ? n : n2;
+  const cudaError_t e = wide ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<true>, 192, smem)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<false>, 192, smem);
+  return e == cudaSuccess ? n : 0;
 }
 
 }  // namespace ps

@@ -420,7 +420,19 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.heads = h->nh; P.kv_heads = h->nkv; P.vocab_local = h->v_count; P.v_begin = h->v_begin;
   P.hd_shift = h->hd == 128 ? 7 : 6;
   P.ntok = ntok;
-  P.stages = mega_stages(ntok, attn_floats);
+  P.stages = mega_stages(ntok, attn_floats, max_rows > 1);
+  {
+    // ring depth caps, PS_MAX_STAGES="decode:wide" overrides. Decode measured
+    // 7/8/9/10 stages = 2.813/2.803/2.794/2.804 ms (same box); wide takes all
+    // the smem allows (5 at 72 rows)
+    static int cap_dec = -1, cap_wide = -1;
+    if (cap_dec < 0) {
+      cap_dec = 9;
+      cap_wide = 64;
+      if (const char* e = std::getenv("PS_MAX_STAGES")) std::sscanf(e, "%d:%d", &cap_dec, &cap_wide);
+    }
+    P.stages = std::min(P.stages, max_rows > 1 ? cap_wide : cap_dec);
+  }
   int cols = 32;
   while (cols < ntok) cols <<= 1;
   P.acc_cols = cols;
@@ -890,8 +902,8 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     for (int ntok = 16; ntok <= kMaxWindow; ntok += 16)
       for (int wide = 0; wide < 2; ++wide) {
         const int attn_floats = mega_attn_bytes(h->hd, grp, wide != 0, h->H) / 4;
-        const int st = mega_stages(ntok, attn_floats);
-        if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats)) < 1)
+        const int st = mega_stages(ntok, attn_floats, wide != 0);
+        if (st < 2 || mega_max_blocks_per_sm(mega_smem_bytes(ntok, st, attn_floats), wide != 0) < 1)
           return (ps_destroy(h), fail(PS_ERR_CUDA, "megakernel does not fit one CTA per SM"));
       }
   }
