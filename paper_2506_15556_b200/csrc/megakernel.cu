@@ -1094,6 +1094,98 @@ struct DefTile {
   int tile, c_first, npieces, r_lo, r_hi, slot0;
 };
 
+// One row t of the vectorised finishing math: features 4*lane .. +3 of
+// `tile` (acc = their fp32 sums, X = the row's residual / RoPE inputs).
+template <class ES>
+__device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, int layer, int n0, int w, int lane,
+                                               int tile, int t, float4 acc, const float* X, ES& es) {
+  const int hd = P.hd, half = hd >> 1;
+  const int f0 = 4 * lane;
+  const int n = tile * 128 + f0;
+  const int r = 0;  // X points at this row's inputs
+  const int rope_row = half * 2;
+  (void)rope_row;
+  if (kind == PH_QKV) {
+    const int rr = n & (hd - 1), pi0 = rr >> 1;  // features f0, f0+1 = dims pi0, pi0+half; f0+2, f0+3 = pi0+1, ..
+    const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
+    float bias[4] = {0.f, 0.f, 0.f, 0.f};
+    if (P.qkv_bias) {
+      const __nv_bfloat16* bp = P.qkv_bias + size_t(layer) * (P.qd + 2 * P.kvd) + n;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) bias[e] = __bfloat162float(bp[e]);
+    }
+    const float rs = es.rstd[t];
+    const float v0 = epi_scale_bias(acc.x, rs, bias[0]), v1 = epi_scale_bias(acc.y, rs, bias[1]);
+    const float v2 = epi_scale_bias(acc.z, rs, bias[2]), v3 = epi_scale_bias(acc.w, rs, bias[3]);
+    float o0 = v0, o1 = v1, o2 = v2, o3 = v3;
+    if (is_q || is_k) {
+      const float4 cs = *reinterpret_cast<const float4*>(X + r * rope_row + 2 * pi0);  // (c, s) of pi0, pi0+1
+      o0 = rope_even(v0, v1, cs.x, cs.y);
+      o1 = rope_odd(v1, v0, cs.x, cs.y);
+      o2 = rope_even(v2, v3, cs.z, cs.w);
+      o3 = rope_odd(v3, v2, cs.z, cs.w);
+    }
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(o0, o2), hi = __floats2bfloat162_rn(o1, o3);
+    const int col = n - rr + pi0;  // original column of dim pi0 (the odd rows are dims + half)
+    __nv_bfloat16* d;
+    if (is_q) {
+      d = P.q + size_t(t) * P.qd + col;
+    } else {
+      const int pos = n0 + t;
+      const int cc = col - P.qd - (is_k ? 0 : P.kvd);
+      const int h = cc >> P.hd_shift;
+      const int page = es.pg[(pos >> 6) - (n0 >> 6)];
+      d = (is_k ? P.kpool : P.vpool) + size_t(layer) * P.g.layer_stride() +
+          ((size_t(page) * P.g.kv_heads + h) * kPage + (pos & (kPage - 1))) * hd + (cc & (hd - 1));
+    }
+    *reinterpret_cast<__nv_bfloat162*>(d) = lo;
+    *reinterpret_cast<__nv_bfloat162*>(d + half) = hi;
+  } else if (kind == PH_GU) {
+    const float rs = es.rstd[t];
+    const float g0 = __fmul_rn(acc.x, rs), u0 = __fmul_rn(acc.y, rs);
+    const float g1 = __fmul_rn(acc.z, rs), u1 = __fmul_rn(acc.w, rs);
+    *reinterpret_cast<__nv_bfloat162*>(P.act + size_t(t) * P.I + tile * 64 + 2 * lane) =
+        __floats2bfloat162_rn(swiglu(g0, u0), swiglu(g1, u1));
+  } else if (kind == PH_O || kind == PH_D) {
+    const float4 xo = *reinterpret_cast<const float4*>(X + r * 128 + f0);
+    const float4 xi = make_float4(__fadd_rn(xo.x, acc.x), __fadd_rn(xo.y, acc.y), __fadd_rn(xo.z, acc.z),
+                                  __fadd_rn(xo.w, acc.w));
+    *reinterpret_cast<float4*>(P.x + size_t(t) * P.H + n) = xi;
+    const bool to_hn = kind == PH_D && layer == P.L - 1;
+    __nv_bfloat16* dst = (to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H) + n;
+    const __nv_bfloat162 b01 = __floats2bfloat162_rn(xi.x, xi.y), b23 = __floats2bfloat162_rn(xi.z, xi.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<const uint32_t*>(&b01);
+    pk.y = *reinterpret_cast<const uint32_t*>(&b23);
+    *reinterpret_cast<uint2*>(dst) = pk;
+    float s0 = __fmul_rn(xi.x, xi.x), s1 = __fmul_rn(xi.y, xi.y), s2 = __fmul_rn(xi.z, xi.z), s3 = __fmul_rn(xi.w, xi.w);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    }
+    const float tot = (s0 + s2) + (s1 + s3);
+    if ((lane & 7) == 0) P.ssq_part[size_t(tile * 4 + (lane >> 3)) * kMaxWindow + t] = tot;
+  } else {  // PH_LM
+    const float rs = es.rstd[t];
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (n + e < P.vocab_local) {
+        const float lv = epi_scale_bias(a4[e], rs, P.lm_bias[P.v_begin + n + e]);
+        if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n + e] = lv;
+        argmax_merge(bv, bi, lv, P.v_begin + n + e);
+      }
+    }
+    warp_argmax(bv, bi);
+    if (lane == 0) argmax_merge(es.am_v[w][t], es.am_i[w][t], bv, bi);
+  }
+}
+
 // Wide passes: a split tile's row share, finalised from shared memory with a
 // vectorised thread map. The pieces' partial rows (contiguous per piece slot)
 // and the per-row inputs (residual rows for O/D, RoPE rows for QKV) are
@@ -1115,7 +1207,6 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
   const int per_row = np * 128 + (has_x ? 128 : has_rope ? rope_row : 0);
   const int batch = cap_floats / per_row;  // >= 8 rows
   const int f0 = 4 * lane;               // this thread's first feature within the tile
-  const int n = T.tile * 128 + f0;
   for (int b0 = T.r_lo; b0 < T.r_hi; b0 += batch) {
     const int nb = min(batch, T.r_hi - b0);
     float* X = S + np * nb * 128;
@@ -1143,85 +1234,7 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
         acc.z += o.z;
         acc.w += o.w;
       }
-      if (kind == PH_QKV) {
-        const int rr = n & (hd - 1), pi0 = rr >> 1;  // features f0, f0+1 = dims pi0, pi0+half; f0+2, f0+3 = pi0+1, ..
-        const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
-        float bias[4] = {0.f, 0.f, 0.f, 0.f};
-        if (P.qkv_bias) {
-          const __nv_bfloat16* bp = P.qkv_bias + size_t(layer) * (P.qd + 2 * P.kvd) + n;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) bias[e] = __bfloat162float(bp[e]);
-        }
-        const float rs = es.rstd[t];
-        const float v0 = epi_scale_bias(acc.x, rs, bias[0]), v1 = epi_scale_bias(acc.y, rs, bias[1]);
-        const float v2 = epi_scale_bias(acc.z, rs, bias[2]), v3 = epi_scale_bias(acc.w, rs, bias[3]);
-        float o0 = v0, o1 = v1, o2 = v2, o3 = v3;
-        if (is_q || is_k) {
-          const float4 cs = *reinterpret_cast<const float4*>(X + r * rope_row + 2 * pi0);  // (c, s) of pi0, pi0+1
-          o0 = rope_even(v0, v1, cs.x, cs.y);
-          o1 = rope_odd(v1, v0, cs.x, cs.y);
-          o2 = rope_even(v2, v3, cs.z, cs.w);
-          o3 = rope_odd(v3, v2, cs.z, cs.w);
-        }
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(o0, o2), hi = __floats2bfloat162_rn(o1, o3);
-        const int col = n - rr + pi0;  // original column of dim pi0 (the odd rows are dims + half)
-        __nv_bfloat16* d;
-        if (is_q) {
-          d = P.q + size_t(t) * P.qd + col;
-        } else {
-          const int pos = n0 + t;
-          const int cc = col - P.qd - (is_k ? 0 : P.kvd);
-          const int h = cc >> P.hd_shift;
-          const int page = es.pg[(pos >> 6) - (n0 >> 6)];
-          d = (is_k ? P.kpool : P.vpool) + size_t(layer) * P.g.layer_stride() +
-              ((size_t(page) * P.g.kv_heads + h) * kPage + (pos & (kPage - 1))) * hd + (cc & (hd - 1));
-        }
-        *reinterpret_cast<__nv_bfloat162*>(d) = lo;
-        *reinterpret_cast<__nv_bfloat162*>(d + half) = hi;
-      } else if (kind == PH_GU) {
-        const float rs = es.rstd[t];
-        const float g0 = __fmul_rn(acc.x, rs), u0 = __fmul_rn(acc.y, rs);
-        const float g1 = __fmul_rn(acc.z, rs), u1 = __fmul_rn(acc.w, rs);
-        *reinterpret_cast<__nv_bfloat162*>(P.act + size_t(t) * P.I + T.tile * 64 + 2 * lane) =
-            __floats2bfloat162_rn(swiglu(g0, u0), swiglu(g1, u1));
-      } else if (kind == PH_O || kind == PH_D) {
-        const float4 xo = *reinterpret_cast<const float4*>(X + r * 128 + f0);
-        const float4 xi = make_float4(__fadd_rn(xo.x, acc.x), __fadd_rn(xo.y, acc.y), __fadd_rn(xo.z, acc.z),
-                                      __fadd_rn(xo.w, acc.w));
-        *reinterpret_cast<float4*>(P.x + size_t(t) * P.H + n) = xi;
-        const bool to_hn = kind == PH_D && layer == P.L - 1;
-        __nv_bfloat16* dst = (to_hn ? P.hn_cache + size_t(n0 + t) * P.H : P.xb + size_t(t) * P.H) + n;
-        const __nv_bfloat162 b01 = __floats2bfloat162_rn(xi.x, xi.y), b23 = __floats2bfloat162_rn(xi.z, xi.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<const uint32_t*>(&b01);
-        pk.y = *reinterpret_cast<const uint32_t*>(&b23);
-        *reinterpret_cast<uint2*>(dst) = pk;
-        float s0 = __fmul_rn(xi.x, xi.x), s1 = __fmul_rn(xi.y, xi.y), s2 = __fmul_rn(xi.z, xi.z), s3 = __fmul_rn(xi.w, xi.w);
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-          s3 += __shfl_xor_sync(0xffffffffu, s3, o);
-        }
-        const float tot = (s0 + s2) + (s1 + s3);
-        if ((lane & 7) == 0) P.ssq_part[size_t(T.tile * 4 + (lane >> 3)) * kMaxWindow + t] = tot;
-      } else {  // PH_LM
-        const float rs = es.rstd[t];
-        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-        float bv = -INFINITY;
-        int bi = 0x7fffffff;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (n + e < P.vocab_local) {
-            const float lv = epi_scale_bias(a4[e], rs, P.lm_bias[P.v_begin + n + e]);
-            if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n + e] = lv;
-            argmax_merge(bv, bi, lv, P.v_begin + n + e);
-          }
-        }
-        warp_argmax(bv, bi);
-        if (lane == 0) argmax_merge(es.am_v[w][t], es.am_i[w][t], bv, bi);
-      }
+      vec_finish_row(P, kind, layer, n0, w, lane, T.tile, t, acc, X + r * (has_x ? 128 : rope_row), es);
     }
     wk_bar();  // the staging area is reused by the next batch / tile
   }
@@ -1623,7 +1636,27 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           tc_fence_after();
           if (tid == 0) stamp(P, p, c, G, 4);
           const uint32_t trow = tmem + b * uint32_t(P.acc_cols) + (uint32_t(q * 32) << 16);
-          if (npieces == 1) {
+          if (kWide && npieces == 1 && (kind == PH_GU || kind == PH_LM) && rows * 512 <= 2 * A.buf) {
+            // whole tile of a wide pass: accumulators -> smem [row][128] (a
+            // transpose through the idle attention buffers), TMEM released, then
+            // the vectorised row math (4 features per thread, as finish_share_vec)
+            ensure_rstd();
+            float* S = reinterpret_cast<float*>(A.K(0));
+            for (int c0 = 0; c0 < rows; c0 += 32) {
+              float v[32];
+              tmem_ld32(trow + c0, v);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j < rows) S[(c0 + j) * 128 + m] = v[j];
+            }
+            tc_fence_before();
+            wk_bar();
+            if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
+            for (int t = w; t < rows; t += 4)
+              vec_finish_row(P, kind, layer, n0, w, lane, tile, t, *reinterpret_cast<const float4*>(S + t * 128 + 4 * lane),
+                             S, es);
+            wk_bar();  // S is reused by the next tile
+          } else if (npieces == 1) {
             ensure_rstd();
             // the next chunk's per-row inputs are in flight while this one finishes
             EpiPre cur, nxt;
