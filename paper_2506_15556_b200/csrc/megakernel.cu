@@ -89,14 +89,8 @@ __device__ __forceinline__ void grid_arrive(unsigned* bar) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
 }
 
-// Spin with relaxed loads (an acquire load would invalidate L1 on every
-// iteration), then one acquire fence once the target is reached.
-__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
+// Acquire-load polling. (Relaxed polling plus one fence after the target is
+// seen measured slower: +1.2% decode, +3% verify — DESIGN.md.)
 __device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
   while (ld_acquire_gpu(bar) < target) {
   }
@@ -1022,7 +1016,7 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
 
 // Finaliser of a split tile in a 1-row pass (decode): own partial (CTA
 // c_first) plus the tagged partials of CTAs c_first+1 .. c_first+npieces-1,
-// summed in CTA order (the order of finish_from_pieces), then the phase's
+// summed in CTA order (the order of the wide finalisation), then the phase's
 // finishing math. The O/D residual load is issued with the partial loads.
 template <class ES>
 __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int layer, int n0, int tile, int m, int q,
@@ -1053,41 +1047,6 @@ __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int
   finish_chunk<1>(P, kind, layer, 1, n0, tile, m, q, lane, 0, v, es, pre);
 }
 
-// Sum a split tile's piece partials (pieces = CTAs c_first.., in CTA order,
-// all loads in flight) for rows [r_lo, r_hi) and run the finishing math.
-template <class ES>
-__device__ __forceinline__ void finish_from_pieces(const MegaParams& P, int kind, int layer, int r_lo, int r_hi, int n0,
-                                                   int tile, int m, int q, int lane, int c_first, int npieces,
-                                                   const Gemm& g, ES& es, int trace_p = -1) {
-  int off[8];
-#pragma unroll
-  off[0] = piece_off_slot(c_first, first_piece_slot(c_first, tile, g), m);
-#pragma unroll
-  for (int pc = 1; pc < 8; ++pc) off[pc] = piece_off_slot(c_first + pc, 0, m);
-  if (trace_p >= 0 && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 3);
-  for (int c0 = r_lo; c0 < r_hi; c0 += 8) {
-    EpiPre pre;
-    epi_load(P, kind, r_hi, n0, tile, m, c0, pre);
-    float tmp[8][8];
-#pragma unroll
-    for (int pc = 0; pc < 8; ++pc)
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        tmp[pc][j] = (pc < npieces && c0 + j < r_hi) ? __ldcg(P.part + off[pc] + size_t(c0 + j) * 128) : 0.f;
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float acc = tmp[0][j];
-#pragma unroll
-      for (int pc = 1; pc < 8; ++pc)
-        if (pc < npieces) acc += tmp[pc][j];
-      v[j] = acc;
-    }
-    if (trace_p >= 0 && c0 == r_lo && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
-    finish_chunk(P, kind, layer, r_hi, n0, tile, m, q, lane, c0, v, es, pre);
-    if (trace_p >= 0 && c0 == r_lo && threadIdx.x == 64) stamp(P, trace_p, blockIdx.x, gridDim.x, 11);
-  }
-}
 
 // A split tile this CTA finalises a row share of (wide passes).
 struct DefTile {
