@@ -1568,6 +1568,10 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         // prefill): every piece publishes without blocking and counts in,
         // then each piece's CTA finalizes its own share of the rows.
         constexpr bool spread = kWide;
+        // wide phases where no CTA range holds a whole tile (QKV, O, D at the
+        // 8B shape): every tile is split, so the finalisation is spread evenly
+        // over the grid after one grid-wide sync instead of per-tile counters
+        const bool all_split = kWide && (g.T + g.G - 1) / g.G < g.KB;
         int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
         if (kind == PH_LM) {
           constexpr int RW = decltype(es)::kRows;
@@ -1578,6 +1582,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           wk_bar();
         }
         const PieceOrder po(kb_lo, kb_hi, g.KB);
+        // the workers are idle until the first accumulator: reduce the staged
+        // RMSNorm partials now rather than on the tail's critical path
+        if (kWide) ensure_rstd();
         for (int pj = 0; pj < po.npieces(); ++pj) {
           int x, piece_hi;
           po.piece(pj, x, piece_hi);
@@ -1659,10 +1666,13 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             wk_bar();
             if (tid == 0) {
               mbar_arrive(acc_empty0 + 8 * b);
-              const unsigned old = atom_add_acq_rel(cnt + tile, 1u);
-              es.flag = old == unsigned(npieces - 1);
+              // (all-split phases sync once per CTA after the piece loop instead)
+              if (!all_split) {
+                const unsigned old = atom_add_acq_rel(cnt + tile, 1u);
+                es.flag = old == unsigned(npieces - 1);
+              }
             }
-            wk_bar();
+            if (!all_split) wk_bar();
             // finalisation is deferred until all of this CTA's pieces are
             // published, so a tile's finaliser never delays the next tile's piece
             if (spread || es.flag) {
@@ -1674,7 +1684,31 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         }
         if (tid == 0) stamp(P, p, c, G, 5);
         ensure_rstd();  // (also completes the staging copies before the buffer is reused)
-        if constexpr (kWide) {
+        if (kWide && all_split) {
+          // every CTA's pieces are out: one grid-wide sync on a per-phase
+          // counter, then CTA c finalises rows [c*I/G, (c+1)*I/G) of the
+          // I = tiles x rows (tile, row) items — at most two tile segments
+          wk_bar();  // every worker's partial stores precede the release below
+          if (tid == 0) {
+            if (c < g.G) grid_arrive(cnt + g.tiles);
+            grid_wait(cnt + g.tiles, unsigned(g.G));
+            stamp(P, p, c, G, 7);
+          }
+          wk_bar();
+          if (tid == 0) stamp(P, p, c, G, 8);
+          const int items = g.tiles * rows;
+          const int a = int((long long)c * items / G), e = int((long long)(c + 1) * items / G);
+          float* stage = reinterpret_cast<float*>(kind == PH_QKV ? A.K(1) : A.K(0));
+          const int cap = (kind == PH_QKV ? A.buf : 2 * A.buf) / 4;
+          for (int i0 = a; i0 < e;) {
+            const int tile = i0 / rows, r0 = i0 - tile * rows, r1 = min(rows, e - tile * rows);
+            const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
+            const DefTile T{tile, c_first, c_last - c_first + 1, r0, r1, first_piece_slot(c_first, tile, g)};
+            finish_share_vec(P, kind, layer, n0, w, lane, T, stage, cap, wbar, wphase, es);
+            i0 = tile * rows + r1;
+          }
+          if (tid == 0) stamp(P, p, c, G, 9);
+        } else if constexpr (kWide) {
           // second pass: wait for the split tiles' pieces, then finalise this
           // CTA's row share of each (every piece's CTA takes a share)
           // Row shares are weighted so that every CTA finalises about the same
