@@ -59,13 +59,16 @@ __device__ __forceinline__ int sk_start(int c, int G, int T) { return (c * T) / 
 // CTA whose k-block range contains global block x
 __device__ __forceinline__ int sk_owner(int x, int G, int T) { return ((x + 1) * G + T - 1) / T - 1; }
 
-// A CTA's k-blocks in order, one piece per tile touched (the natural order
-// keeps DRAM access sequential; finishing order was measured not to matter).
+// A CTA's k-blocks, one piece per tile touched, in natural order (keeps
+// DRAM access sequential). Processing the split pieces first, so their
+// finalisation could overlap whole tiles' mainloop, was measured slower
+// (verify +1%: the delayed whole-tile epilogues land on the phase tail).
 struct PieceOrder {
-  int lo, hi, KB, t_first;
-  __device__ __forceinline__ PieceOrder(int lo_, int hi_, int KB_) : lo(lo_), hi(hi_), KB(KB_), t_first(lo_ / KB_) {}
-  __device__ __forceinline__ int npieces() const { return hi > lo ? (hi - 1) / KB - t_first + 1 : 0; }
-  __device__ __forceinline__ int block(int i) const { return lo + i; }
+  int lo, hi, KB, t_first, np;
+  __device__ __forceinline__ PieceOrder(int lo_, int hi_, int KB_) : lo(lo_), hi(hi_), KB(KB_), t_first(lo_ / KB_) {
+    np = hi > lo ? (hi - 1) / KB - t_first + 1 : 0;
+  }
+  __device__ __forceinline__ int npieces() const { return np; }
   __device__ __forceinline__ void piece(int j, int& plo, int& phi) const {
     plo = max(lo, (t_first + j) * KB);
     phi = min(hi, (t_first + j + 1) * KB);
@@ -1285,35 +1288,65 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           const int xrow = kind == PH_LM ? xrow_lm : 0;
           const uint32_t tx = kTileABytes + b_bytes;
           const int pre = min(min(nk, ST), P.pre_max);
-          for (int i = 0; i < pre; ++i) {
-            const uint32_t s = (it + i) % ST, ph = ((it + i) / ST) & 1;
+          // Block cursor over the pieces in processing order, and the ring
+          // slot/parity, advanced incrementally: this single thread issues
+          // every load of the CTA, so no per-block divisions.
+          struct Cursor {
+            const PieceOrder& po;
+            int KB, j, x, hi, tile, kb;
+            __device__ __forceinline__ void start(int jj) {
+              j = jj;
+              po.piece(j, x, hi);
+              tile = x / KB;
+              kb = x - tile * KB;
+            }
+            __device__ __forceinline__ void next() {
+              ++x;
+              if (++kb == KB) {
+                kb = 0;
+                ++tile;
+              }
+              if (x == hi && j + 1 < po.npieces()) start(j + 1);
+            }
+          };
+          Cursor cur{po, g.KB, 0, 0, 0, 0, 0}, bcur{po, g.KB, 0, 0, 0, 0, 0};
+          if (nk > 0) {
+            cur.start(0);
+            bcur.start(0);
+          }
+          uint32_t s0 = it % ST, ph0 = (it / ST) & 1;  // slot and parity of this phase's first block
+          uint32_t s = s0, ph = ph0;
+          auto bump = [&](uint32_t& ss, uint32_t& pp) {
+            if (++ss == uint32_t(ST)) {
+              ss = 0;
+              pp ^= 1u;
+            }
+          };
+          for (int i = 0; i < pre; ++i, cur.next(), bump(s, ph)) {
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
-            const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
-            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
+            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, cur.kb * kBK, cur.tile * 128, pol_stream);
           }
           // HBM is idle while the grid finishes the previous phase (its tail,
           // and all of ATTN): the next P.pf[kind] boxes of this CTA's range
           // beyond the ring go to L2 now, and the ring reads them from there
           for (int i = pre; i < nk && i < pre + P.pf[kind]; ++i) {
-            const int x = po.block(i);
+            const int x = kb_lo + i;
             tma_prefetch_2d(wm, (x % g.KB) * kBK, (x / g.KB) * 128);
           }
           grid_wait(P.bar, unsigned(G) * unsigned(p - p_first + 1));  // activations of this phase are complete
           stamp(P, p, c, G, 0);
           fence_proxy_async_global();
-          for (int i = 0; i < pre; ++i) {
-            const uint32_t s = (it + i) % ST;
-            const int x = po.block(i), kb = x % g.KB;
-            tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
+          {
+            uint32_t sb = s0, pb = ph0;
+            for (int i = 0; i < pre; ++i, bcur.next(), bump(sb, pb))
+              tma_load_2d(smem_u32(b_tile(sb)), xm, full0 + 8 * sb, bcur.kb * kBK, xrow);
           }
-          for (int i = pre; i < nk; ++i) {
-            const uint32_t s = (it + i) % ST, ph = ((it + i) / ST) & 1;
+          for (int i = pre; i < nk; ++i, cur.next(), bump(s, ph)) {
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             mbar_expect_tx(full0 + 8 * s, tx);
-            const int x = po.block(i), tile = x / g.KB, kb = x % g.KB;
-            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, kb * kBK, tile * 128, pol_stream);
-            tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, kb * kBK, xrow);
+            tma_load_2d_hint(smem_u32(a_tile(s)), wm, full0 + 8 * s, cur.kb * kBK, cur.tile * 128, pol_stream);
+            tma_load_2d(smem_u32(b_tile(s)), xm, full0 + 8 * s, cur.kb * kBK, xrow);
           }
           stamp(P, p, c, G, 12);
           it += nk;
@@ -1327,6 +1360,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       if (!P.ctx->stop) {
         const uint32_t idesc = idesc_bf16(P.ntok);
         uint32_t it = 0, acc_it = 0;
+        uint32_t ms = 0, mph = 0;  // ring slot / parity of block `it`, advanced incrementally
         for (int p = p_first; p < nphases; ++p) {
           const int kind = phase_kind(p, P.L);
           if (kind == PH_ATTN || kind == PH_FINAL) continue;
@@ -1341,7 +1375,11 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             tc_fence_after();
             const uint32_t dcol = tmem + b * uint32_t(P.acc_cols);
             for (int y = x; y < piece_hi; ++y, ++it) {
-              const uint32_t s = it % ST, ph = (it / ST) & 1;
+              const uint32_t s = ms, ph = mph;
+              if (++ms == uint32_t(ST)) {
+                ms = 0;
+                mph ^= 1u;
+              }
               mbar_wait(full0 + 8 * s, ph);
               tc_fence_after();
               const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
@@ -1581,6 +1619,56 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           }
           wk_bar();
         }
+        // wide, not all-split: finalise this CTA's row shares of its split tiles
+        bool finalized = false;
+        auto finalize_split_tiles = [&]() {
+          // second pass: wait for the split tiles' pieces, then finalise this
+          // CTA's row share of each (every piece's CTA takes a share)
+          // Row shares are weighted so that every CTA finalises about the same
+          // number of rows in total: a CTA with two split tiles (its first and
+          // last piece) takes half-weight shares of each.
+          auto split_pieces = [&](int cc) {
+            const int lo = sk_start(cc, g.G, g.T), hi = sk_start(cc + 1, g.G, g.T);
+            const int t0 = lo / g.KB, t1 = (hi - 1) / g.KB;
+            const int first = (lo != t0 * g.KB || hi < (t0 + 1) * g.KB) ? 1 : 0;
+            const int last = (t1 != t0 && hi != (t1 + 1) * g.KB) ? 1 : 0;
+            return first + last;
+          };
+          auto def_of = [&](int tile) {
+            const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
+            const int npieces = c_last - c_first + 1;
+            int wsum = 0, wbefore = 0, wmine = 0;
+            for (int pc = 0; pc < npieces; ++pc) {
+              const int wt = split_pieces(c_first + pc) > 1 ? 1 : 2;
+              if (c_first + pc < c) wbefore += wt;
+              if (c_first + pc == c) wmine = wt;
+              wsum += wt;
+            }
+            return DefTile{tile, c_first, npieces, wbefore * rows / wsum, (wbefore + wmine) * rows / wsum,
+                           first_piece_slot(c_first, tile, g)};
+          };
+          // dtile1 is only set once dtile0 is
+          const int nd = (dtile0 >= 0) + (dtile1 >= 0);
+          DefTile D[2] = {dtile0 >= 0 ? def_of(dtile0) : DefTile{0, 0, 1, 0, 0, 0},
+                          dtile1 >= 0 ? def_of(dtile1) : DefTile{0, 0, 1, 0, 0, 0}};
+          if (tid == 0) {
+            if (nd > 0) grid_wait(cnt + D[0].tile, unsigned(D[0].npieces));
+            if (nd > 1) grid_wait(cnt + D[1].tile, unsigned(D[1].npieces));
+            stamp(P, p, c, G, 7);
+          }
+          wk_bar();
+          if (tid == 0) stamp(P, p, c, G, 8);
+          // staging area: both attention buffers, except in QKV where buffer 0
+          // holds the next ATTN phase's prefetched keys
+          float* stage = reinterpret_cast<float*>(kind == PH_QKV ? A.K(1) : A.K(0));
+          const int cap = (kind == PH_QKV ? A.buf : 2 * A.buf) / 4;
+#pragma unroll
+          for (int d = 0; d < 2; ++d)
+            if (d < nd && D[d].r_lo < D[d].r_hi)
+              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, wbar, wphase, es);
+          if (tid == 0) stamp(P, p, c, G, 9);
+          finalized = true;
+        };
         const PieceOrder po(kb_lo, kb_hi, g.KB);
         // the workers are idle until the first accumulator: reduce the staged
         // RMSNorm partials now rather than on the tail's critical path
@@ -1708,52 +1796,8 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             i0 = tile * rows + r1;
           }
           if (tid == 0) stamp(P, p, c, G, 9);
-        } else if constexpr (kWide) {
-          // second pass: wait for the split tiles' pieces, then finalise this
-          // CTA's row share of each (every piece's CTA takes a share)
-          // Row shares are weighted so that every CTA finalises about the same
-          // number of rows in total: a CTA with two split tiles (its first and
-          // last piece) takes half-weight shares of each.
-          auto split_pieces = [&](int cc) {
-            const int lo = sk_start(cc, g.G, g.T), hi = sk_start(cc + 1, g.G, g.T);
-            const int t0 = lo / g.KB, t1 = (hi - 1) / g.KB;
-            const int first = (lo != t0 * g.KB || hi < (t0 + 1) * g.KB) ? 1 : 0;
-            const int last = (t1 != t0 && hi != (t1 + 1) * g.KB) ? 1 : 0;
-            return first + last;
-          };
-          auto def_of = [&](int tile) {
-            const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
-            const int npieces = c_last - c_first + 1;
-            int wsum = 0, wbefore = 0, wmine = 0;
-            for (int pc = 0; pc < npieces; ++pc) {
-              const int wt = split_pieces(c_first + pc) > 1 ? 1 : 2;
-              if (c_first + pc < c) wbefore += wt;
-              if (c_first + pc == c) wmine = wt;
-              wsum += wt;
-            }
-            return DefTile{tile, c_first, npieces, wbefore * rows / wsum, (wbefore + wmine) * rows / wsum,
-                           first_piece_slot(c_first, tile, g)};
-          };
-          // dtile1 is only set once dtile0 is
-          const int nd = (dtile0 >= 0) + (dtile1 >= 0);
-          DefTile D[2] = {dtile0 >= 0 ? def_of(dtile0) : DefTile{0, 0, 1, 0, 0, 0},
-                          dtile1 >= 0 ? def_of(dtile1) : DefTile{0, 0, 1, 0, 0, 0}};
-          if (tid == 0) {
-            if (nd > 0) grid_wait(cnt + D[0].tile, unsigned(D[0].npieces));
-            if (nd > 1) grid_wait(cnt + D[1].tile, unsigned(D[1].npieces));
-            stamp(P, p, c, G, 7);
-          }
-          wk_bar();
-          if (tid == 0) stamp(P, p, c, G, 8);
-          // staging area: both attention buffers, except in QKV where buffer 0
-          // holds the next ATTN phase's prefetched keys
-          float* stage = reinterpret_cast<float*>(kind == PH_QKV ? A.K(1) : A.K(0));
-          const int cap = (kind == PH_QKV ? A.buf : 2 * A.buf) / 4;
-#pragma unroll
-          for (int d = 0; d < 2; ++d)
-            if (d < nd && D[d].r_lo < D[d].r_hi)
-              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, wbar, wphase, es);
-          if (tid == 0) stamp(P, p, c, G, 9);
+        } else if (kWide && !finalized) {
+          finalize_split_tiles();
         }
         if (tid == 0) stamp(P, p, c, G, 6);
         if (kind == PH_LM) {
