@@ -121,6 +121,26 @@ def test_batch_invariance_bitwise(tiny, small_bf16, which):
     assert np.array_equal(one.view(np.uint32), step.view(np.uint32))
 
 
+# GU and LM wide enough that CTA ranges hold whole tiles (GU: 152 tiles,
+# LM: 250 > 148 SMs): the wide kernel's non-all-split finalisation (per-tile
+# counters, weighted shares) and its smem-transposed whole-tile epilogue run,
+# which the small shape (every tile split) never reaches.
+MID_BF16 = small_shape("mid-bf16", intermediate=9728, vocab=32000)
+
+
+@pytest.mark.parametrize("n", [72, 100])
+def test_batch_invariance_bitwise_whole_tiles(n):
+    """As above on MID_BF16; 100 rows also takes the > 80-row fallbacks (RMSNorm
+    partials without staging, TMEM-lane whole-tile epilogues)."""
+    lm = B200LM(MID_BF16, seed=3, max_seq=512)
+    try:
+        toks = rand_tokens(np.random.default_rng(4), lm.vocab_size, n)
+        one, step = _rows_one_pass_vs_stepwise(lm, toks)
+        assert np.array_equal(one.view(np.uint32), step.view(np.uint32))
+    finally:
+        lm.close()
+
+
 def test_decode_graph_matches_eager_and_forward(small_bf16):
     toks = rand_tokens(np.random.default_rng(2), SMALL_BF16.vocab, 30)
     fused = [t for t, _ in small_bf16.decode_greedy_fused(toks, 40)]
