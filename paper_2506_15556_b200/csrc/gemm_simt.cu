@@ -24,7 +24,9 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict
   const int nvec = ksplit >> 2;
   const float4* w0 = reinterpret_cast<const float4*>(W + size_t(n0) * K + kbeg);
   const float4* w1 = reinterpret_cast<const float4*>(W + size_t(n0 + 1) * K + kbeg);
-  for (int tt = 0; tt < rows; tt += TT) {
+  // blockIdx.z takes every gridDim.z-th chunk of TT tokens (more CTAs for
+  // narrow N; the per-output arithmetic does not depend on the chunking)
+  for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
     const int nt = min(TT, rows - tt);
     __syncthreads();
     for (int e = threadIdx.x; e < TT * nvec; e += 256) {
@@ -72,7 +74,7 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
     cudaFuncSetAttribute(gemm_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(N / 16, splits);
+  dim3 grid(N / 16, splits, max_rows <= 1 ? 1 : (max_rows + 15) / 16);
   if (max_rows <= 1)
     gemm_f32_kernel<1><<<grid, 256, size_t(ksplit) * 4, st>>>(ctx, X, ldx, W, part, N, K, ksplit);
   else
