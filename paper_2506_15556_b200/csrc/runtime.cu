@@ -724,7 +724,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
   if (const char* env = std::getenv("PS_TC_SPLITS")) std::sscanf(env, "%d,%d,%d,%d", &force_splits[0], &force_splits[1],
                                                                  &force_splits[2], &force_splits[3]);
   int gemm_idx = 0;
-  const int tile_n = h->bf16 ? kTileTc : 16, kgran = h->bf16 ? 64 : 128, maxk = h->bf16 ? 0 : 2048;
+  const int tile_n = h->bf16 ? kTileTc : 16, kgran = h->bf16 ? 64 : 32, maxk = h->bf16 ? 0 : 2048;
   size_t part_elems = 0;
   for (int l = 0; l < h->L; ++l) {
     Layer& ly = h->layers[l];
