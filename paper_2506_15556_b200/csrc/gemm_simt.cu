@@ -96,9 +96,13 @@ __global__ void __launch_bounds__(256) lmhead_f32_kernel(PassCtx* ctx, const flo
   const int rows = ctx->rows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = H >> 2;
-  const int tile = blockIdx.x;
+  // blockIdx.x = tile * Z + z: the Z token chunks of a vocab tile are
+  // neighbouring CTAs, so the tile's weights are read from DRAM once and
+  // from L2 by the others
+  const int ntiles = (v_count + kLmTileF32 - 1) / kLmTileF32;
+  const int Z = int(gridDim.x) / ntiles, tile = blockIdx.x / Z, z = blockIdx.x % Z;
   const float* X = hn_cache + size_t(ctx->n0) * H;
-  for (int tt = 0; tt < rows; tt += TT) {
+  for (int tt = z * TT; tt < rows; tt += TT * Z) {
     const int nt = min(TT, rows - tt);
     __syncthreads();
     for (int e = threadIdx.x; e < TT * nvec; e += 256) {
@@ -171,10 +175,11 @@ void launch_lmhead_f32(const PassCtx* ctx, int max_rows, const float* hn_cache, 
   if (max_rows <= 1)
     lmhead_f32_kernel<1><<<tiles, 256, size_t(hidden) * 4, st>>>(c, hn_cache, W, bias, v_begin, v_count, hidden,
                                                                  am_val, am_idx, logits_out, ld_logits);
-  else
-    lmhead_f32_kernel<16><<<tiles, 256, size_t(hidden) * 16 * 4, st>>>(c, hn_cache, W, bias, v_begin, v_count,
-                                                                       hidden, am_val, am_idx, logits_out,
-                                                                       ld_logits);
+  else {
+    const int Z = (max_rows + 15) / 16;  // token chunks per vocab tile (gridDim.x = tiles * Z)
+    lmhead_f32_kernel<16><<<tiles * Z, 256, size_t(hidden) * 16 * 4, st>>>(
+        c, hn_cache, W, bias, v_begin, v_count, hidden, am_val, am_idx, logits_out, ld_logits);
+  }
 }
 
 }  // namespace ps
