@@ -870,7 +870,9 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     h->sms = dev_sms > 0 ? dev_sms : 148;
     h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128 * 2);  // room for u64 tagged partials
     h->mega_epoch = h->dalloc<unsigned>(1);
-    h->mega_max_tiles = (std::max(std::max(h->qd + 2 * h->kvd, 2 * h->I), std::max(h->H, h->v_count)) + 127) / 128;
+    // per-phase counter block: one counter per tile plus the all-split
+    // phases' grid-sync counter at index `tiles` (megakernel.cu)
+    h->mega_max_tiles = (std::max(std::max(h->qd + 2 * h->kvd, 2 * h->I), std::max(h->H, h->v_count)) + 127) / 128 + 1;
     h->mega_cnt_words = 64 + size_t(3 + 5 * h->L) * h->mega_max_tiles;
     h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
