@@ -128,7 +128,7 @@ def test_batch_invariance_bitwise(tiny, small_bf16, which):
 MID_BF16 = small_shape("mid-bf16", intermediate=9728, vocab=32000)
 
 
-@pytest.mark.parametrize("n", [72, 100])
+@pytest.mark.parametrize("n", [72, 100, 200])
 def test_batch_invariance_bitwise_whole_tiles(n):
     """As above on MID_BF16; 100 rows also takes the > 80-row fallbacks (RMSNorm
     partials without staging, TMEM-lane whole-tile epilogues)."""
