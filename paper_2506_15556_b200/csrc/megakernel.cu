@@ -105,10 +105,13 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-// trace slots per (phase, CTA): 0 producer passed barrier, 1 workers passed
-// barrier, 2 workers finished the phase, 3 MMA issue finished, 4 workers saw
-// the last accumulator, 5 workers published all partials, 6 workers done with
-// the deferred finalisation
+// PS_TRACE slots per (phase, CTA), read by tools/trace_mega.py: 0 producer
+// passed the barrier, 1 workers passed it, 2 workers finished the phase,
+// 4 workers saw the last accumulator, 5 workers published all partials,
+// 6 finalisation done, 7/8 split-tile counters (or the grid sync) passed,
+// 9 shares finalised, 7-11 attention milestones in ATTN phases, 12 producer
+// issued its last load, 13 MMA issued its last block, 14/15 attention S and
+// softmax of the first unit
 constexpr int kTraceSlots = 16;
 __device__ __forceinline__ void stamp(const MegaParams& P, int p, int c, int G, int slot) {
   if (P.trace) P.trace[(size_t(p) * G + c) * kTraceSlots + slot] = gtime();
@@ -356,9 +359,9 @@ __device__ __forceinline__ void finish_chunk(const MegaParams& P, int kind, int 
 
 // rstd of every row of the pass from the per-tile sums of squares of the
 // previous RESID phase (or the embed rstd), one warp per row, fixed tree.
-// Rows are processed kRstdBatch at a time with every load in flight (a wide
-// pass has up to 256 rows; one L2 round trip per row was the verify pass's
-// largest worker cost).
+// Rows are processed kRstdBatch at a time with every load in flight. Wide
+// passes of up to kRstdStageRows rows stage the partials in shared memory
+// instead (rstd_stage_issue / rstd_stage_reduce, same tree).
 constexpr int kRstdBatch = 4;
 template <class ES>
 __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, int rows, int w, int lane, ES& es) {
