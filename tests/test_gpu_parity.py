@@ -141,6 +141,29 @@ def test_batch_invariance_bitwise_whole_tiles(n):
         lm.close()
 
 
+def test_long_context_bitwise_and_decode(small_bf16):
+    """Contexts past 8 KV pages take the general attention merge (more than 8
+    pages per row) and several attention units per CTA; a 700-token prompt scored
+    in 256-row chunks agrees bitwise with 1-row passes over its tail, and the
+    graph-replayed decode continues with the forward argmax."""
+    lm = small_bf16
+    toks = rand_tokens(np.random.default_rng(5), lm.vocab_size, 700)
+    lm.discard_after(0)
+    block, _, _ = lm.forward(toks)
+    one = np.stack([np.asarray(block.row_for(p)) for p in range(690, 700)])
+    lm.discard_after(0)
+    lm.forward(toks[:690])
+    step = []
+    for n in range(691, 701):
+        b, _, _ = lm.forward(toks[:n])
+        step.append(np.asarray(b.row_for(n - 1)))
+    assert np.array_equal(one.view(np.uint32), np.stack(step).view(np.uint32))
+    lm.discard_after(0)
+    fused = [t for t, _ in lm.decode_greedy_fused(toks, 6)]
+    seq = greedy_decode(lm, toks, max_new=6, stop=None)
+    assert seq[len(toks):] == fused[: len(seq) - len(toks)]
+
+
 def test_decode_graph_matches_eager_and_forward(small_bf16):
     toks = rand_tokens(np.random.default_rng(2), SMALL_BF16.vocab, 30)
     fused = [t for t, _ in small_bf16.decode_greedy_fused(toks, 40)]
