@@ -159,6 +159,27 @@ def cpu_port_timing(shape, sample_s: float, threads: int, context: int = 128, wi
             "verify_samples": len(ver), "setup_s": setup_s, "threads": threads}
 
 
+def ttfs_roofline(results, pass_floor_ms: float) -> dict:
+    """TTFS fraction = Σ floors of the passes in the TTFS window
+    / measured TTFS. Every pass that computes rows streams all weights once, so
+    its floor is the weight-bytes floor; prefix hits (cost 0) have none."""
+    fracs, floors = [], []
+    for res in results:
+        ev = res.events
+        t0 = next((e.payload["arrival_ms"] for e in ev if e.kind == "chunk_received" and e.payload.get("is_final")),
+                  None)
+        ts = next((e.t_ms for e in ev if e.kind == "sentence_emitted"), None)
+        if t0 is None or ts is None or ts <= t0:
+            continue
+        fl = sum(pass_floor_ms for e in ev if e.kind in ("verify", "generate_step") and t0 < e.t_ms <= ts
+                 and e.payload.get("cost_ms", 0.0) > 0.0)
+        floors.append(fl)
+        fracs.append(fl / (ts - t0))
+    if not fracs:
+        return {}
+    return {"p50_ttfs_floor_ms": statistics.median(floors), "p50_ttfs_roofline_frac": statistics.median(fracs)}
+
+
 def conv_rate_from_passes(t: dict, mix: dict) -> float:
     per_conv_ms = mix["decode_rows"] * t["decode_ms"] + mix["extend_rows"] / 72.0 * t["verify_ms"]
     return 1000.0 / per_conv_ms
@@ -300,7 +321,8 @@ def main():
                            "count": len(verify_nonzero)},
         "decode_step_ms": {"p50": step_ms, "count": len(lm.decode_ms),
                            "hbm_floor_ms": lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3},
-        "ttfs_ms": {k: v for k, v in ttfs.items() if "ttfs" in k or "nfetfs" in k},
+        "ttfs_ms": {**{k: v for k, v in ttfs.items() if "ttfs" in k or "nfetfs" in k},
+                    **ttfs_roofline(results, lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3)},
         "turns": len(records),
         "roofline": {"bound": "hbm",
                      "kernel": ("mega_kernel: whole 1-row decode pass, one persistent tcgen05 kernel" if dom == "whole_pass"
