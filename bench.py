@@ -318,7 +318,11 @@ def main():
         "e2e": {"value": world * n_conv / (vals["elapsed"] / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps},
         "verify_step_ms": {"p50": statistics.median(verify_nonzero) if verify_nonzero else None,
-                           "count": len(verify_nonzero)},
+                           "count": len(verify_nonzero),
+                           # a verify window streams the same weights once: same HBM floor
+                           "hbm_floor_ms": lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3,
+                           "roofline_frac": (lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3
+                                             / statistics.median(verify_nonzero)) if verify_nonzero else None},
         "decode_step_ms": {"p50": step_ms, "count": len(lm.decode_ms),
                            "hbm_floor_ms": lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3},
         "ttfs_ms": {**{k: v for k, v in ttfs.items() if "ttfs" in k or "nfetfs" in k},
