@@ -165,6 +165,7 @@ struct MegaParams {
   unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
   int pre_max;              // weight stages issued ahead of a phase barrier (<= stages)
   int pf[8];                // per phase kind: weight boxes L2-prefetched ahead of the phase barrier
+  int gcap[8];              // per phase kind: cap on the stream-K CTA count (0 = none; PS_SK_G)
 };
 // attention staging of the megakernel (see AttnSmem in megakernel.cu): decode
 // passes one unit buffer of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]

@@ -51,6 +51,7 @@ __device__ __forceinline__ Gemm gemm_of(const MegaParams& P, int kind) {
   g.T = g.tiles * g.KB;
   // pieces per tile <= ceil(KB / (T/G)) + 1 <= 8  <=>  G <= 7 * tiles
   g.G = min(min(int(gridDim.x), 7 * g.tiles), g.T);  // and T >= G: no empty CTA ranges
+  if (P.gcap[kind] > 0) g.G = min(g.G, P.gcap[kind]);  // tuning hook (same for every pass width)
   return g;
 }
 

@@ -497,6 +497,16 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
       pre_init = true;
     }
     P.pre_max = max_rows > 1 ? pre_wide : pre_dec;
+    // stream-K CTA caps "q:o:gu:d:lm" (identical for decode and wide passes, so
+    // the per-row arithmetic stays pass-width independent)
+    static int gcap[5] = {0, 0, 0, 0, 0};
+    static bool gcap_init = false;
+    if (!gcap_init) {
+      if (const char* e = std::getenv("PS_SK_G"))
+        std::sscanf(e, "%d:%d:%d:%d:%d", &gcap[0], &gcap[1], &gcap[2], &gcap[3], &gcap[4]);
+      gcap_init = true;
+    }
+    for (int k = 0; k < 5; ++k) P.gcap[1 + (k == 0 ? 0 : k + 1)] = gcap[k];
     for (int k = 0; k < 5; ++k) P.pf[1 + (k == 0 ? 0 : k + 1)] = pf[k];  // kinds QKV=1, O=3, GU=4, D=5, LM=6
   }
   // 1-row passes use only the barrier words (the per-phase tile counters
