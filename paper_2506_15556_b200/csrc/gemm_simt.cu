@@ -14,6 +14,7 @@ template <int TT>
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict__ ctx, const float* __restrict__ X,
                                                        int ldx, const float* __restrict__ W, float* __restrict__ part,
                                                        int N, int K, int ksplit) {
+  pdl_enter();
   extern __shared__ float4 xs4[];
   if (ctx->stop) return;
   const int rows = ctx->rows;
@@ -76,9 +77,9 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
   }
   dim3 grid(N / 16, splits, max_rows <= 1 ? 1 : (max_rows + 15) / 16);
   if (max_rows <= 1)
-    gemm_f32_kernel<1><<<grid, 256, size_t(ksplit) * 4, st>>>(ctx, X, ldx, W, part, N, K, ksplit);
+    launch_pdl(gemm_f32_kernel<1>, dim3(grid), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part, N, K, ksplit);
   else
-    gemm_f32_kernel<16><<<grid, 256, size_t(ksplit) * 16 * 4, st>>>(ctx, X, ldx, W, part, N, K, ksplit);
+    launch_pdl(gemm_f32_kernel<16>, dim3(grid), dim3(256), size_t(ksplit) * 16 * 4, st, ctx, X, ldx, W, part, N, K, ksplit);
 }
 
 // LM head: 64 vocab ids per CTA (8 warps x 2 rows x 4 passes), fused
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(256) lmhead_f32_kernel(PassCtx* ctx, const flo
                                                          int v_begin, int v_count, int H, float* __restrict__ am_val,
                                                          int* __restrict__ am_idx, float* __restrict__ logits_out,
                                                          int ld_logits) {
+  pdl_enter();
   extern __shared__ float4 xs4[];
   __shared__ float bv[8][TT];
   __shared__ int bi[8][TT];
@@ -173,11 +175,11 @@ void launch_lmhead_f32(const PassCtx* ctx, int max_rows, const float* hn_cache, 
   const int tiles = (v_count + kLmTileF32 - 1) / kLmTileF32;
   PassCtx* c = const_cast<PassCtx*>(ctx);
   if (max_rows <= 1)
-    lmhead_f32_kernel<1><<<tiles, 256, size_t(hidden) * 4, st>>>(c, hn_cache, W, bias, v_begin, v_count, hidden,
+    launch_pdl(lmhead_f32_kernel<1>, dim3(tiles), dim3(256), size_t(hidden) * 4, st, c, hn_cache, W, bias, v_begin, v_count, hidden,
                                                                  am_val, am_idx, logits_out, ld_logits);
   else {
     const int Z = (max_rows + 15) / 16;  // token chunks per vocab tile (gridDim.x = tiles * Z)
-    lmhead_f32_kernel<16><<<tiles * Z, 256, size_t(hidden) * 16 * 4, st>>>(
+    launch_pdl(lmhead_f32_kernel<16>, dim3(tiles * Z), dim3(256), size_t(hidden) * 16 * 4, st, 
         c, hn_cache, W, bias, v_begin, v_count, hidden, am_val, am_idx, logits_out, ld_logits);
   }
 }

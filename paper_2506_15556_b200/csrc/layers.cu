@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(PassCtx* ctx, const int
                                                          const int* __restrict__ argmax_pos,
                                                          const T* __restrict__ embed, float* __restrict__ x,
                                                          T* __restrict__ xn, int H, float eps) {
+  pdl_enter();
   __shared__ float red[32];
   __shared__ int s_tok;
   const int t = blockIdx.x;
@@ -60,7 +61,7 @@ template <typename T>
 void launch_embed_norm(const PassCtx* ctx, int max_rows, const int* tok_in, int* tokens_dev,
                        const int* argmax_pos, const T* embed, float* x, T* xn, int hidden, float eps,
                        cudaStream_t st) {
-  embed_norm_kernel<T><<<max_rows, 256, 0, st>>>(const_cast<PassCtx*>(ctx), tok_in, tokens_dev,
+  launch_pdl(embed_norm_kernel<T>, dim3(max_rows), dim3(256), 0, st, const_cast<PassCtx*>(ctx), tok_in, tokens_dev,
                                                   argmax_pos, embed, x, xn, hidden, eps);
 }
 
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __rest
                                                            T* __restrict__ kpool, T* __restrict__ vpool,
                                                            const int* __restrict__ page_table, KvGeom g,
                                                            int layer, int heads) {
+  pdl_enter();
   const int t = blockIdx.x;
   if (ctx->stop || t >= ctx->rows) return;
   const int pos = ctx->n0 + t;
@@ -124,7 +126,7 @@ template <typename T>
 void launch_qkv_finalize(const PassCtx* ctx, int max_rows, const float* part, int splits, int ldp,
                          const T* bias, const float2* rope, T* q, T* kpool, T* vpool,
                          const int* page_table, KvGeom g, int layer, int heads, cudaStream_t st) {
-  qkv_finalize_kernel<T><<<max_rows, 128, 0, st>>>(ctx, part, splits, ldp, bias, rope, q, kpool, vpool,
+  launch_pdl(qkv_finalize_kernel<T>, dim3(max_rows), dim3(128), 0, st, ctx, part, splits, ldp, bias, rope, q, kpool, vpool,
                                                    page_table, g, layer, heads);
 }
 
@@ -138,6 +140,7 @@ __global__ void attention_page_kernel(const PassCtx* __restrict__ ctx, const T* 
                                       const int* __restrict__ page_table, KvGeom g, int layer, int heads,
                                       int max_splits, float scale, float* __restrict__ o_part,
                                       float* __restrict__ ml_part) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int t = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
   if (ctx->stop || t >= ctx->rows) return;
@@ -198,6 +201,7 @@ template <typename T>
 __global__ void attention_combine_kernel(const PassCtx* __restrict__ ctx, int heads, int hd, int max_splits,
                                          const float* __restrict__ o_part, const float* __restrict__ ml_part,
                                          T* __restrict__ out) {
+  pdl_enter();
   const int t = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   if (ctx->stop || t >= ctx->rows) return;
   const int nsplit = (ctx->n0 + t) / kPage + 1;
@@ -229,9 +233,9 @@ void launch_attention(const PassCtx* ctx, int max_rows, int max_pos, const T* q,
   }
   const float scale = float(1.0 / sqrt(double(hd)));
   dim3 grid(max_rows, g.kv_heads, max_splits);
-  attention_page_kernel<T><<<grid, grp * 32, smem, st>>>(ctx, q, kpool, vpool, page_table, g, layer, heads,
+  launch_pdl(attention_page_kernel<T>, dim3(grid), dim3(grp * 32), smem, st, ctx, q, kpool, vpool, page_table, g, layer, heads,
                                                          max_splits, scale, o_part, ml_part);
-  attention_combine_kernel<T><<<dim3(max_rows, heads), hd, 0, st>>>(ctx, heads, hd, max_splits, o_part,
+  launch_pdl(attention_combine_kernel<T>, dim3(dim3(max_rows, heads)), dim3(hd), 0, st, ctx, heads, hd, max_splits, o_part,
                                                                      ml_part, attn_out);
 }
 
@@ -243,6 +247,7 @@ __global__ void __launch_bounds__(256) residual_norm_kernel(const PassCtx* __res
                                                             const float* __restrict__ part, int splits,
                                                             T* __restrict__ xn, T* __restrict__ hn_cache, int H,
                                                             float eps) {
+  pdl_enter();
   __shared__ float red[32];
   const int t = blockIdx.x;
   if (ctx->stop || t >= ctx->rows) return;
@@ -267,13 +272,14 @@ template <typename T>
 void launch_residual_norm(const PassCtx* ctx, int max_rows, float* x, const float* part, int splits,
                           int ldp, T* xn, T* hn_cache, int hidden, float eps, cudaStream_t st) {
   (void)ldp;
-  residual_norm_kernel<T><<<max_rows, 256, 0, st>>>(ctx, x, part, splits, xn, hn_cache, hidden, eps);
+  launch_pdl(residual_norm_kernel<T>, dim3(max_rows), dim3(256), 0, st, ctx, x, part, splits, xn, hn_cache, hidden, eps);
 }
 
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void swiglu_kernel(const PassCtx* __restrict__ ctx, const float* __restrict__ part, int splits,
                               T* __restrict__ act, int I) {
+  pdl_enter();
   const int t = blockIdx.y;
   if (ctx->stop || t >= ctx->rows) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -294,7 +300,7 @@ template <typename T>
 void launch_swiglu(const PassCtx* ctx, int max_rows, const float* part, int splits, int ldp, T* act,
                    int inter, cudaStream_t st) {
   (void)ldp;
-  swiglu_kernel<T><<<dim3((inter + 255) / 256, max_rows), 256, 0, st>>>(ctx, part, splits, act, inter);
+  launch_pdl(swiglu_kernel<T>, dim3(dim3((inter + 255) / 256, max_rows)), dim3(256), 0, st, ctx, part, splits, act, inter);
 }
 
 // ---------------------------------------------------------------------------
@@ -304,6 +310,7 @@ __global__ void __launch_bounds__(256) argmax_reduce_kernel(PassCtx* ctx, const 
                                                             const int* __restrict__ am_idx, int tiles,
                                                             int* __restrict__ argmax_pos,
                                                             unsigned long long* __restrict__ packed_out) {
+  pdl_enter();
   __shared__ float sv[8];
   __shared__ int si[8];
   const int t = blockIdx.x;
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(256) argmax_reduce_kernel(PassCtx* ctx, const 
 
 void launch_argmax_reduce(const PassCtx* ctx, int max_rows, const float* am_val, const int* am_idx,
                           int tiles, int* argmax_pos, unsigned long long* packed_out, cudaStream_t st) {
-  argmax_reduce_kernel<<<max_rows, 256, 0, st>>>(const_cast<PassCtx*>(ctx), am_val, am_idx, tiles, argmax_pos,
+  launch_pdl(argmax_reduce_kernel, dim3(max_rows), dim3(256), 0, st, const_cast<PassCtx*>(ctx), am_val, am_idx, tiles, argmax_pos,
                                                  packed_out);
 }
 
@@ -436,10 +443,11 @@ void launch_shard_unpack(PassCtx* ctx, const unsigned long long* keys, unsigned 
 }
 
 __global__ void advance_kernel(PassCtx* ctx) {
+  pdl_enter();
   if (!ctx->stop) { ctx->n0 += 1; ctx->step += 1; }
 }
 
-void launch_advance(PassCtx* ctx, cudaStream_t st) { advance_kernel<<<1, 1, 0, st>>>(ctx); }
+void launch_advance(PassCtx* ctx, cudaStream_t st) { launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, ctx); }
 
 #define PS_INST(T)                                                                                       \
   template void launch_embed_norm<T>(const PassCtx*, int, const int*, int*, const int*, const T*, float*, \
