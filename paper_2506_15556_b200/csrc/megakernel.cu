@@ -28,9 +28,14 @@ namespace ps {
 namespace {
 
 enum Phase : int { PH_EMBED = 0, PH_QKV, PH_ATTN, PH_O, PH_GU, PH_D, PH_LM, PH_FINAL };
-constexpr int kWorkers = 128;  // warps 2..5
+// Worker threads: warps 2.. of the CTA (4 warps in the decode kernel, 6 in the
+// wide kernel). TMEM-lane work (one warp per lane quadrant) stays on the first
+// four; row-parallel work (vectorised finalisation, merges, RMSNorm
+// reductions) spreads over all of them.
+#define kWorkers (int(blockDim.x) - 64)
+#define kWorkerWarps ((int(blockDim.x) - 64) >> 5)
 
-__device__ __forceinline__ void wk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void wk_bar() { asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x - 64) : "memory"); }
 
 struct Gemm {
   int N, KB, T;  // rows, k-blocks per tile, total k-blocks
@@ -165,8 +170,8 @@ __device__ __forceinline__ float swiglu(float gate, float up) {
 template <int RW>
 struct EpiSmemT {
   static constexpr int kRows = RW;
-  float am_v[4][RW];  // LM head: running (max, id) per warp quadrant and row
-  int am_i[4][RW];
+  float am_v[6][RW];  // LM head: running (max, id) per worker warp (or quadrant) and row
+  int am_i[6][RW];
   float red_v[4][8];
   int red_i[4][8];
   float rstd[RW];
@@ -372,11 +377,12 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
   }
   // 4 quadrant partials per tile; lane sums entries lane, lane+32, ... in order
   const int nparts = 4 * (P.H / 128);  // <= 4 * 64
-  for (int t0 = w; t0 < rows; t0 += 4 * kRstdBatch) {
+  const int nw = kWorkerWarps;
+  for (int t0 = w; t0 < rows; t0 += nw * kRstdBatch) {
     float vals[kRstdBatch][8];
 #pragma unroll
     for (int r = 0; r < kRstdBatch; ++r) {
-      const int t = t0 + 4 * r;
+      const int t = t0 + nw * r;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = lane + 32 * u;
@@ -385,7 +391,7 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
     }
 #pragma unroll
     for (int r = 0; r < kRstdBatch; ++r) {
-      const int t = t0 + 4 * r;
+      const int t = t0 + nw * r;
       float a = 0.f;
 #pragma unroll
       for (int u = 0; u < 8; ++u) a += vals[r][u];
@@ -457,7 +463,7 @@ __device__ __forceinline__ bool rstd_stage_fits(const MegaParams& P, const AttnS
 __device__ __forceinline__ void rstd_stage_issue(const MegaParams& P, const AttnSmem& A, int rows, int w, int lane) {
   float* S = reinterpret_cast<float*>(A.K(1));
   const int nparts = 4 * (P.H / 128), ld = rstd_stage_ld(rows);
-  for (int e = w; e < nparts; e += 4)
+  for (int e = w; e < nparts; e += kWorkerWarps)
     for (int v = 4 * lane; v < ld; v += 128) cp_async16(S + e * ld + v, P.ssq_part + size_t(e) * kMaxWindow + v);
 }
 template <class ES>
@@ -465,7 +471,7 @@ __device__ __forceinline__ void rstd_stage_reduce(const MegaParams& P, const Att
                                                   ES& es) {
   const float* S = reinterpret_cast<const float*>(A.K(1));
   const int nparts = 4 * (P.H / 128), ld = rstd_stage_ld(rows);
-  for (int g0 = w * 8; g0 < rows; g0 += 32) {
+  for (int g0 = w * 8; g0 < rows; g0 += 8 * kWorkerWarps) {
     float a[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -1190,7 +1196,7 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
     }
     mbar_wait(wbar, wphase);
     wphase ^= 1u;
-    for (int r = w; r < nb; r += 4) {
+    for (int r = w; r < nb; r += kWorkerWarps) {
       const int t = b0 + r;
       float4 acc = *reinterpret_cast<const float4*>(S + r * 128 + f0);
       for (int pc = 1; pc < np; ++pc) {
@@ -1215,7 +1221,10 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
 // allocation free of the other's paths; the per-row arithmetic is the same
 // source, so a row is bitwise identical in both (tests/test_gpu_parity.py).
 template <bool kWide>
-__global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ MegaParams P) {
+__global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid_constant__ MegaParams P) {
+  // the launch shape is fixed per instantiation: lets the inlined helpers fold
+  // the worker count (kWorkers, kWorkerWarps, wk_bar) to a constant
+  __builtin_assume(blockDim.x == (kWide ? 256u : 192u));
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // [full x kMaxStages][empty x kMaxStages][acc_full x 2][acc_empty x 2][workers' staging]
   __shared__ uint64_t bars[2 * kMaxStages + 4 + 1];
@@ -1432,7 +1441,9 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       uint4* ob = reinterpret_cast<uint4*>(P.xb + size_t(t) * P.H);
       float* xr = P.x + size_t(t) * P.H;
       float ss = 0.f;
-      for (int cc = tid; cc < P.H / 8; cc += kWorkers) {
+      // the first 4 worker warps only, stride 128: rstd0's sum tree is the same
+      // in both instantiations
+      for (int cc = tid; w < 4 && cc < P.H / 8; cc += 128) {
         const uint4 raw = e[cc];
         ob[cc] = raw;
         const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(&raw);
@@ -1444,7 +1455,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         }
       }
       ss = warp_sum(ss);
-      if (lane == 0) es.red_v[w][0] = ss;
+      if (lane == 0 && w < 4) es.red_v[w][0] = ss;
       wk_bar();
       if (tid == 0) P.rstd0[t] = 1.0f / sqrtf((((es.red_v[0][0] + es.red_v[1][0]) + es.red_v[2][0]) + es.red_v[3][0]) / float(P.H) + P.eps);
       wk_bar();
@@ -1492,7 +1503,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
       if (kind == PH_FINAL) {
         // argmax of every row over the per-CTA partials of the LM phase;
         // rows are spread over CTAs (t = c, c+G, ...), one warp per row
-        for (int t = c * 4 + w; t < rows; t += 4 * G) {
+        for (int t = c * kWorkerWarps + w; t < rows; t += kWorkerWarps * G) {
           float bv = -INFINITY;
           int bi = 0x7fffffff;
           float vv[8];
@@ -1563,7 +1574,8 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         }
         wk_bar();
         const int items = rows * P.heads;
-        for (int it = c * 4 + w; it < items; it += 4 * G) attn_merge_one(P, n0, it / P.heads, it % P.heads, lane);
+        for (int it = c * kWorkerWarps + w; it < items; it += kWorkerWarps * G)
+          attn_merge_one(P, n0, it / P.heads, it % P.heads, lane);
         if (tid == 0) stamp(P, p, c, G, 11);
       } else if (kind == PH_ATTN) {
         // decode: about one unit per CTA, so one operand buffer (the smem it
@@ -1617,7 +1629,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
         int dtile0 = -1, dtile1 = -1;  // split tiles whose finalisation is deferred (<= 2 per CTA)
         if (kind == PH_LM) {
           constexpr int RW = decltype(es)::kRows;
-          for (int e = tid; e < 4 * RW; e += kWorkers) {
+          for (int e = tid; e < 6 * RW; e += kWorkers) {
             es.am_v[e / RW][e % RW] = -INFINITY;
             es.am_i[e / RW][e % RW] = 0x7fffffff;
           }
@@ -1700,7 +1712,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             // the vectorised row math (4 features per thread, as finish_share_vec)
             ensure_rstd();
             float* S = reinterpret_cast<float*>(A.K(0));
-            for (int c0 = 0; c0 < rows; c0 += 32) {
+            for (int c0 = 0; w < 4 && c0 < rows; c0 += 32) {  // TMEM lane quadrants: first 4 warps
               float v[32];
               tmem_ld32(trow + c0, v);
 #pragma unroll
@@ -1710,7 +1722,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             tc_fence_before();
             wk_bar();
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
-            for (int t = w; t < rows; t += 4)
+            for (int t = w; t < rows; t += kWorkerWarps)
               vec_finish_row(P, kind, layer, n0, w, lane, tile, t, *reinterpret_cast<const float4*>(S + t * 128 + 4 * lane),
                              S, es);
             wk_bar();  // S is reused by the next tile
@@ -1718,8 +1730,8 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             ensure_rstd();
             // the next chunk's per-row inputs are in flight while this one finishes
             EpiPre cur, nxt;
-            epi_load(P, kind, rows, n0, tile, m, 0, cur);
-            for (int c0 = 0; c0 < rows; c0 += 8) {
+            if (w < 4) epi_load(P, kind, rows, n0, tile, m, 0, cur);
+            for (int c0 = 0; w < 4 && c0 < rows; c0 += 8) {  // TMEM lane quadrants: first 4 warps
               if (c0 + 8 < rows) epi_load(P, kind, rows, n0, tile, m, c0 + 8, nxt);
               float v[8];
               tmem_ld8(trow + c0, v);
@@ -1747,7 +1759,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
           } else {
             float* mine = P.part + piece_off_slot(c, pj == 0 ? 0 : 1, m);
-            for (int c0 = 0; c0 < rows; c0 += 32) {
+            for (int c0 = 0; w < 4 && c0 < rows; c0 += 32) {  // TMEM lane quadrants: first 4 warps
               float v[32];
               tmem_ld32(trow + c0, v);
 #pragma unroll
@@ -1810,7 +1822,7 @@ __global__ void __launch_bounds__(192, 1) mega_kernel(const __grid_constant__ Me
           for (int t = tid; t < rows; t += kWorkers) {
             float bv = es.am_v[0][t];
             int bi = es.am_i[0][t];
-            for (int qq = 1; qq < 4; ++qq) argmax_merge(bv, bi, es.am_v[qq][t], es.am_i[qq][t]);
+            for (int qq = 1; qq < 6; ++qq) argmax_merge(bv, bi, es.am_v[qq][t], es.am_i[qq][t]);
             P.am_val[size_t(c) * kMaxWindow + t] = bv;
             P.am_idx[size_t(c) * kMaxWindow + t] = bi;
           }
@@ -1876,7 +1888,7 @@ cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cuda
   if (const cudaError_t e = mega_set_smem_attr(); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(wide ? 256 : 192);  // wide: 6 worker warps (the register budget stays 255)
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr1[1];
@@ -1890,7 +1902,7 @@ cudaError_t launch_mega(const MegaParams& P, bool wide, int grid, int smem, cuda
 int mega_max_blocks_per_sm(int smem, bool wide) {
   if (mega_set_smem_attr() != cudaSuccess) return 0;
   int n = 0;
-  const cudaError_t e = wide ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<true>, 192, smem)
+  const cudaError_t e = wide ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<true>, 256, smem)
                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mega_kernel<false>, 192, smem);
   return e == cudaSuccess ? n : 0;
 }
