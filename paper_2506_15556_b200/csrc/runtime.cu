@@ -273,6 +273,16 @@ void* offset_ptr(ps_handle* h, void* base, size_t elems) {
   return static_cast<unsigned char*>(base) + elems * h->esz;
 }
 
+// A blocking copy ordered with the runtime stream. (A plain cudaMemcpy runs on
+// the legacy stream, which does not order with the non-blocking runtime
+// stream: e.g. the LM-bias upload in ps_create could land BEFORE the
+// stream-ordered zero-fill of its allocation, which then wiped it.)
+cudaError_t copy_sync(ps_handle* h, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, h->st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(h->st);
+}
+
 cudaError_t copy_async(ps_handle* h, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
   if (kind == cudaMemcpyHostToDevice) h->stats.h2d_bytes += int64_t(bytes);
   if (kind == cudaMemcpyDeviceToHost) h->stats.d2h_bytes += int64_t(bytes);
@@ -722,7 +732,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     std::vector<float> b(V, 0.f);
     b[0] = c.eos_bias;
     for (int i = 1; i < 4; ++i) b[i] = c.term_bias;
-    cudaMemcpy(h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
+    copy_sync(h, h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
   }
   h->layers.resize(h->L);
   if (h->bf16 && c.qkv_bias) {
@@ -898,7 +908,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       std::memcpy(&wm[4 * l + 3], h->layers[l].d.tm.bytes, sizeof(CUtensorMap));
     }
     std::memcpy(&wm[4 * h->L], h->tm_head.bytes, sizeof(CUtensorMap));
-    cudaMemcpy(h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice);
+    copy_sync(h, h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice);
     std::vector<CUtensorMap> xm(size_t(kMaxWindow / 16) * 4);
     for (int k = 0; k < kMaxWindow / 16; ++k) {
       const ActDescs* ad = act_descs(h, 16 * (k + 1));
@@ -908,7 +918,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       std::memcpy(&xm[4 * k + 2], ad->act.bytes, sizeof(CUtensorMap));
       std::memcpy(&xm[4 * k + 3], ad->hn.bytes, sizeof(CUtensorMap));
     }
-    cudaMemcpy(h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
+    copy_sync(h, h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
     // every pass width must fit one CTA per SM (co-residency of the grid)
     const int grp = h->nh / h->nkv;
     for (int ntok = 16; ntok <= kMaxWindow; ntok += 16)
@@ -929,10 +939,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
         const double a = double(p) * inv;
         tab[p * half + i] = make_float2(float(std::cos(a)), float(std::sin(a)));
       }
-    cudaMemcpy(h->rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice);
+    copy_sync(h, h->rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice);
     std::vector<unsigned char> tm(V, 0);
     tm[1] = tm[2] = tm[3] = 1;
-    cudaMemcpy(h->term_mask, tm.data(), V, cudaMemcpyHostToDevice);
+    copy_sync(h, h->term_mask, tm.data(), V, cudaMemcpyHostToDevice);
   }
   if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return (ps_destroy(h), fail(PS_ERR_CUDA, "device initialisation failed"));
@@ -1174,7 +1184,7 @@ int ps_argmax_rows(ps_handle* h, int32_t first, int32_t n, int32_t* out) {
 int ps_set_terminators(ps_handle* h, const uint8_t* mask, int32_t vocab) {
   if (!h || !mask || vocab != h->V) return fail(PS_ERR_INVALID, "terminator mask must cover the vocabulary");
   CK(cudaSetDevice(h->cfg.device));
-  CK(cudaMemcpy(h->term_mask, mask, vocab, cudaMemcpyHostToDevice));
+  CK(copy_sync(h, h->term_mask, mask, vocab, cudaMemcpyHostToDevice));
   return PS_OK;
 }
 
@@ -1190,7 +1200,7 @@ int ps_read_weights(ps_handle* h, int32_t tid, int64_t offset, int64_t count, fl
         const int64_t src = offset + i, r = src / e.cols, c = src % e.cols;
         const int64_t dr = e.perm.dst(int(r));
         const int64_t take = std::min<int64_t>(count - i, e.cols - c);
-        CK(cudaMemcpy(row.data(), static_cast<uint16_t*>(e.ptr) + dr * e.cols + c, 2 * take, cudaMemcpyDeviceToHost));
+        CK(copy_sync(h, row.data(), static_cast<uint16_t*>(e.ptr) + dr * e.cols + c, 2 * take, cudaMemcpyDeviceToHost));
         for (int64_t k = 0; k < take; ++k) {
           uint32_t b = uint32_t(row[k]) << 16;
           std::memcpy(out + i + k, &b, 4);
@@ -1201,13 +1211,13 @@ int ps_read_weights(ps_handle* h, int32_t tid, int64_t offset, int64_t count, fl
     }
     if (h->bf16) {
       std::vector<uint16_t> tmp(count);
-      CK(cudaMemcpy(tmp.data(), static_cast<uint16_t*>(e.ptr) + offset, 2 * count, cudaMemcpyDeviceToHost));
+      CK(copy_sync(h, tmp.data(), static_cast<uint16_t*>(e.ptr) + offset, 2 * count, cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < count; ++i) {
         uint32_t b = uint32_t(tmp[i]) << 16;
         std::memcpy(out + i, &b, 4);
       }
     } else {
-      CK(cudaMemcpy(out, static_cast<float*>(e.ptr) + offset, 4 * count, cudaMemcpyDeviceToHost));
+      CK(copy_sync(h, out, static_cast<float*>(e.ptr) + offset, 4 * count, cudaMemcpyDeviceToHost));
     }
     return PS_OK;
   }
@@ -1287,7 +1297,7 @@ int ps_trace(ps_handle* h, uint64_t* out, int64_t cap, int32_t* nphases, int32_t
   *nphases = 3 + 5 * h->L;
   *ctas = h->sms;
   const int64_t n = int64_t(*nphases) * h->sms * 16;
-  if (out) CK(cudaMemcpy(out, h->mega_trace, sizeof(uint64_t) * std::min<int64_t>(cap, n), cudaMemcpyDeviceToHost));
+  if (out) CK(copy_sync(h, out, h->mega_trace, sizeof(uint64_t) * std::min<int64_t>(cap, n), cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 
@@ -1324,7 +1334,7 @@ int ps_shard_keys(ps_handle* h, int32_t first, int32_t n, uint64_t* out) {
     return fail(PS_ERR_INVALID, "rows outside the resident sequence");
   if (h->cfg.vocab_shards <= 1) return fail(PS_ERR_INVALID, "not a vocab-sharded instance");
   CK(cudaSetDevice(h->cfg.device));
-  CK(cudaMemcpy(out, h->keys_pos + first, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  CK(copy_sync(h, out, h->keys_pos + first, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 
