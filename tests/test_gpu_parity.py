@@ -141,6 +141,23 @@ def test_batch_invariance_bitwise_whole_tiles(n):
         lm.close()
 
 
+def test_batch_invariance_and_agreement_hd64():
+    """head_dim 64 on the bf16 path (two heads per 128-row QKV tile, 64-dim RoPE
+    rows, half-warp attention merges): bitwise batch invariance and agreement with
+    the bf16-emulating oracle."""
+    shape = small_shape("small-bf16-hd64", heads=8, kv_heads=2, head_dim=64)
+    lm = B200LM(shape, seed=2, max_seq=512)
+    try:
+        toks = rand_tokens(np.random.default_rng(6), lm.vocab_size, 72)
+        one, step = _rows_one_pass_vs_stepwise(lm, toks)
+        assert np.array_equal(one.view(np.uint32), step.view(np.uint32))
+        ref = DecoderOracle(shape.as_dict(), seed=2)
+        _, want = ref.extend(toks)
+        assert np.abs(one - want).max() < 0.06
+    finally:
+        lm.close()
+
+
 def test_long_context_bitwise_and_decode(small_bf16):
     """Contexts past 8 KV pages take the general attention merge (more than 8
     pages per row) and several attention units per CTA; a 700-token prompt scored
