@@ -1,6 +1,6 @@
 """Decode-step / verify time for values of one environment knob.
 
-    python tools/sweep_splits.py [--var NAME] value...   (default NAME: PS_TC_SPLITS)
+    python tools/sweep_splits.py [--var NAME] value...   (default NAME: PS_SK_G; also PS_MAX_STAGES, PS_PF_WIDE, ...)
 """
 import os, subprocess, sys, json
 from pathlib import Path
@@ -26,7 +26,7 @@ for i in range(5):
 print("RESULT", statistics.median(ms), statistics.median(v))
 ''' % ROOT
 args = sys.argv[1:]
-var = "PS_TC_SPLITS"
+var = "PS_SK_G"
 if args[:1] == ["--var"]:
     var, args = args[1], args[2:]
 for combo in args:
