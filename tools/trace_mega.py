@@ -25,7 +25,8 @@ def grab():
              ctypes.byref(ct))
     tr = buf.reshape(np_.value, ct.value, NS).astype(np.float64)
     t0 = tr[0, :, 2][tr[0, :, 2] > 0].min()
-    return np.where(tr > 0, (tr - t0) / 1000.0, np.nan)
+    # slots this pass did not write still hold an earlier pass's stamps: drop them
+    return np.where(tr >= t0, (tr - t0) / 1000.0, np.nan)
 
 def report(tr, label):
     agg = collections.defaultdict(lambda: collections.defaultdict(list))
