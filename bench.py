@@ -4,28 +4,33 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
 Workload (config c5 of BASELINE.json): synthetic MT-Bench/Lmsys-length
-conversations on the Llama-3-8B shape (bf16, random init, measured-cost
-SimClock), sharded one stream per GPU (weak scaling: every rank simulates
-`--conv-per-step` conversations per step). A "step" = that batch of
-conversations through the public API (`run_conversation` -> verify / decode
--> B200LM -> C-ABI -> CUDA). One JSON line on rank 0:
+conversations on the Llama-3-8B shape (bf16, random init), run through the
+reference's own loop (`specstream.run_conversation` with the fused verifiers
+bound in, paper_2506_15556_b200/fused.py) on `B200LM`. One process per GPU,
+ranks claim conversations from a shared work queue (no per-pass collective).
 
-* value: conversations/s over the device time of every pass (inputs are
-  token ids already resident in pinned host memory; host orchestration
-  excluded) — max over ranks;
-* e2e: conversations/s over the CUDA-event-bracketed wall time of the steps
-  (host Python loop, H2D token copies and D2H argmax reads included);
-* verify-step latency (p50 ms of the fused verify calls), decode-step
-  latency, simulated p50 TTFS under measured cost — the BASELINE metrics;
-* roofline for the dominant kernel class (gate/up tcgen05 GEMM), measured
-  with CUDA events around each launch (ps_profile_decode);
-* cpu_baseline: the oracle decoder (numpy fp32, all host threads) timed on a
-  bounded sample of the same 8B-shape passes, converted to conversations/s
-  with this run's pass mix.
+Two phases, because the two BASELINE metrics need two clocks:
 
-`--impl reference` times the reference's CPU path for this workload: the
-reference has no decoder (its LM is a hash table, lm.py:216-243), so its
-stand-in is the oracle port (oracle/decoder.py), rank 0 only.
+1. conversations/s (the JSON `value`): the reference's modeled cost
+   (`LatencyModel`, lm.py:40-57) drives the SimClock, exactly like the
+   reference's `simulate` command; every decision then depends only on the
+   model's argmaxes, so the pass schedule of a conversation is deterministic.
+   Step s = conversations [s*P*N, (s+1)*P*N) (P = --conv-per-step per rank).
+   value = conversations / max-over-ranks device time of every pass;
+   e2e = conversations / max-over-ranks CUDA-event wall time of the steps
+   (host Python, H2D token copies and D2H argmax reads included).
+   The per-conversation pass schedule is compared with the committed one
+   (bench_data/, tools/make_schedule.py) that the reference arm prices.
+2. latency (rank 0): measured cost — every pass charges its CUDA-event ms —
+   over a fixed set of conversations: p50 verify-step latency, decode-step
+   latency, p50/p90 simulated TTFS, each with its HBM-roofline fraction.
+
+`--impl reference` (and `cpu_baseline`): the reference has no decoder (its LM
+is a hash table, lm.py:216-243), so its CPU path for this workload is the
+oracle decoder (oracle/decoder.py, numpy fp32, all host threads) pricing the
+SAME pass schedule: per-pass CPU times t(rows) = a + b*rows fitted on a
+bounded sample of 8B-shape passes, summed over the timed conversations'
+committed schedule (same conversation ids, same config dict as this arm).
 """
 
 from __future__ import annotations
@@ -43,15 +48,13 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "conversations/sec (c5 predict-and-verify simulation); verify-step latency; simulated p50 TTFS"
+METRIC = ("conversations/sec (c5 predict-and-verify simulation, modeled-cost schedule); "
+          "verify-step latency; simulated p50 TTFS")
 UNIT = "conversations/s"
-
-# pass mix of one c5 conversation on the 8B shape, measured by this bench
-# (bench.py --steps 8, 2026-10-17; refreshed from the live run when available)
-DEFAULT_PASS_MIX = {"decode_rows": 180.0, "extend_rows": 420.0}
+TTFS_CONVERSATIONS = range(1000, 1012)  # measured-cost latency phase (rank 0)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=4)
@@ -60,8 +63,29 @@ def parse():
     ap.add_argument("--conv-per-step", type=int, default=2)
     ap.add_argument("--shape", default="llama-3-8b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def schedule_path(shape_name: str) -> Path:
+    return ROOT / "bench_data" / f"c5_schedule_{shape_name}.json"
+
+
+def timed_ids(world: int, per: int, warmup: int, steps: int) -> tuple[int, int]:
+    return warmup * per * world, (warmup + steps) * per * world
+
+
+def workload_config(args, world: int) -> dict:
+    """The config dict both arms print (identical by construction)."""
+    lo, hi = timed_ids(world, args.conv_per_step, args.warmup, args.steps)
+    return {"workload": "c5: synthetic MT-Bench/Lmsys-length conversations through the reference's run_turn, "
+                        "Llama-3-8B shape, bf16, modeled-cost SimClock (LatencyModel 30 ms + 0.5 ms/token)",
+            "shape": args.shape, "timed_conversation_ids": [lo, hi], "conversations_per_rank_per_step":
+                args.conv_per_step, "chunk_words": 2, "max_response_tokens": 64, "rate_chars_per_min": 600.0,
+            "schedule": str(schedule_path(args.shape).relative_to(ROOT)),
+            "l2": "inputs larger than L2 (15 GB of weights streamed per pass)",
+            "parallelism": f"{world} conversation shards, dynamic work queue, no per-pass collective"}
 
 
 class ClockSampler:
@@ -124,15 +148,30 @@ def dist_env():
     return world, rank, device
 
 
-def cpu_port_timing(shape, sample_s: float, threads: int, context: int = 128, window: int = 72) -> dict:
-    """Oracle decoder (numpy fp32, BLAS on `threads` host threads) per-pass times at `shape`.
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    Every layer streams layer 0's weights (share_layer_weights): the same bytes
-    and FLOPs per pass as the full model, without generating 8B values on the
-    host. Returns ms for a 1-row decode pass and a `window`-row verify pass.
-    """
+
+# -- CPU pricing of a pass schedule ---------------------------------------------------------
+
+def cpu_pass_model(shape, sample_s: float, threads: int, context: int = 128,
+                   widths=(1, 8, 32, 72)) -> dict:
+    """Oracle decoder (numpy fp32, BLAS on `threads` host threads) per-pass times at `shape`:
+    t_decode = the median 1-row pass, and t(rows) = a + b*rows for wider passes (least
+    squares over the per-width medians of the wider widths).
+
+    Every layer streams layer 0's weights (share_layer_weights): the same bytes and FLOPs
+    per pass as the full model, without generating 8B values on the host. Passes run over
+    a `context`-token resident prefix (attention is < 1% of a CPU pass at this length)."""
     import numpy as np
     from oracle.decoder import DecoderOracle
+
     t0 = time.perf_counter()
     d = dict(shape.as_dict())
     d["mode"] = 0  # fp32 arithmetic: no bf16 rounding emulation in the timed port
@@ -140,23 +179,49 @@ def cpu_port_timing(shape, sample_s: float, threads: int, context: int = 128, wi
     rng = np.random.default_rng(0)
     m.extend([int(t) for t in rng.integers(4, shape.vocab, context)])
     setup_s = time.perf_counter() - t0
-    dec, ver = [], []
+    samples = {w: [] for w in widths}
     deadline = time.perf_counter() + sample_s
-    base = len(m.tokens)
-    while time.perf_counter() < deadline or len(dec) < 2 or len(ver) < 1:
+    i = 0
+    while time.perf_counter() < deadline or any(len(v) < 2 for v in samples.values()):
+        w = widths[i % len(widths)]
+        i += 1
+        m.truncate(context)
         t = time.perf_counter()
-        m.extend([int(rng.integers(4, shape.vocab))])
-        dec.append((time.perf_counter() - t) * 1e3)
-        if len(dec) % 4 == 0:
-            m.truncate(base)
-            t = time.perf_counter()
-            m.extend([int(x) for x in rng.integers(4, shape.vocab, window)])
-            ver.append((time.perf_counter() - t) * 1e3)
-            m.truncate(base)
-        if len(dec) > 64:
+        m.extend([int(x) for x in rng.integers(4, shape.vocab, w)])
+        samples[w].append((time.perf_counter() - t) * 1e3)
+        if w == 1:  # decode passes are the bulk of a schedule: sample them more densely
+            for _ in range(3):
+                t = time.perf_counter()
+                m.extend([int(rng.integers(4, shape.vocab))])
+                samples[1].append((time.perf_counter() - t) * 1e3)
+        if i > 400:
             break
-    return {"decode_ms": statistics.median(dec), "verify_ms": statistics.median(ver), "decode_samples": len(dec),
-            "verify_samples": len(ver), "setup_s": setup_s, "threads": threads}
+    ys = {w: statistics.median(samples[w]) for w in widths}
+    wide = [w for w in widths if w > 1]
+    b, a = np.polyfit(np.array(wide, dtype=np.float64), np.array([ys[w] for w in wide]), 1)
+    return {"decode_ms": float(ys[1]), "a_ms": float(a), "b_ms_per_row": float(b),
+            "median_ms": {str(w): float(y) for w, y in ys.items()},
+            "samples": {str(w): len(v) for w, v in samples.items()}, "setup_s": setup_s, "threads": threads,
+            "context": context}
+
+
+def cpu_schedule_ms(model: dict, entries) -> float:
+    """CPU time of schedule entries [passes, rows, decode_passes, extend_passes]:
+    decode passes at t_decode, extend passes at a + b*rows."""
+    return sum(model["decode_ms"] * e[2] + model["a_ms"] * e[3] + model["b_ms_per_row"] * (e[1] - e[2])
+               for e in entries)
+
+
+def load_schedule(shape_name: str) -> dict:
+    p = schedule_path(shape_name)
+    return json.loads(p.read_text()) if p.exists() else {"conversations": {}}
+
+
+def summarize_schedule(entries) -> list:
+    """[(ctx, rows)] of one conversation -> [n_passes, rows, decode_passes, extend_passes]."""
+    rows = sum(r for _, r in entries)
+    dec = sum(1 for _, r in entries if r == 1)
+    return [len(entries), rows, dec, len(entries) - dec]
 
 
 def ttfs_roofline(results, pass_floor_ms: float) -> dict:
@@ -180,10 +245,7 @@ def ttfs_roofline(results, pass_floor_ms: float) -> dict:
     return {"p50_ttfs_floor_ms": statistics.median(floors), "p50_ttfs_roofline_frac": statistics.median(fracs)}
 
 
-def conv_rate_from_passes(t: dict, mix: dict) -> float:
-    per_conv_ms = mix["decode_rows"] * t["decode_ms"] + mix["extend_rows"] / 72.0 * t["verify_ms"]
-    return 1000.0 / per_conv_ms
-
+# -- reference arm ------------------------------------------------------------------------------
 
 def reference_arm(args):
     world, rank, _ = dist_env()
@@ -192,78 +254,99 @@ def reference_arm(args):
     from paper_2506_15556_b200.shapes import SHAPES
     shape = SHAPES[args.shape]
     threads = os.cpu_count() or 1
+    sched = load_schedule(shape.name)["conversations"]
+    lo, hi = timed_ids(world, args.conv_per_step, args.warmup, args.steps)
+    ids = [f"c{i:05d}" for i in range(lo, hi)]
+    have = [sched[c] for c in ids if c in sched]
+    if not have:
+        print(json.dumps({"impl": "reference", "unavailable": f"no committed pass schedule for {args.shape}"}))
+        return
     per_step = max(2.0, args.cpu_sample_s / max(1, args.steps + args.warmup))
-    times = []
-    t = None
+    models = []
     for i in range(args.warmup + args.steps):
-        t = cpu_port_timing(shape, per_step if i >= args.warmup else 1.0, threads)
+        m = cpu_pass_model(shape, per_step if i >= args.warmup else 1.0, threads)
         if i >= args.warmup:
-            times.append(t)
-    dec = statistics.median(x["decode_ms"] for x in times)
-    ver = statistics.median(x["verify_ms"] for x in times)
-    rate = conv_rate_from_passes({"decode_ms": dec, "verify_ms": ver}, DEFAULT_PASS_MIX)
-    sample = (f"oracle port (numpy fp32, {threads} threads) at the {shape.name} shape: median of 1-row decode and "
-              f"72-row verify passes over a 128-token context; conversations/s = 1 / (decode_rows*t_dec + "
-              f"extend_rows/72*t_verify) with the c5 pass mix {DEFAULT_PASS_MIX}")
+            models.append(m)
+    model = {k: statistics.median(m[k] for m in models) for k in ("decode_ms", "a_ms", "b_ms_per_row")}
+    # conversations the schedule lacks are priced at the mean of those it has
+    total_ms = cpu_schedule_ms(model, have) * len(ids) / len(have)
+    rate = len(ids) / (total_ms / 1e3)
+    sample = (f"oracle port (numpy fp32, {threads} threads, {cpu_model()}) at the {shape.name} shape: "
+              f"decode pass {model['decode_ms']:.1f} ms, wider passes {model['a_ms']:.1f} ms + "
+              f"{model['b_ms_per_row']:.2f} ms/row (fit on 8/32/72 rows), over a 128-token context, summed over "
+              f"the committed pass schedule of conversations "
+              f"{lo}..{hi - 1} ({len(have)}/{len(ids)} scheduled)")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "c5: synthetic MT-Bench/Lmsys-length conversations", "shape": shape.name},
-            "verify_step_ms": ver, "decode_step_ms": dec,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights, synthetic vocabulary and conversations)",
+            "config": workload_config(args, world),
+            "verify_step_ms": model["a_ms"] + 72 * model["b_ms_per_row"],
+            "decode_step_ms": model["decode_ms"],
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse()
+# -- our arm --------------------------------------------------------------------------------------
+
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return reference_arm(args)
     world, rank, local = dist_env()
     import torch
     torch.cuda.set_device(local)
     if world > 1:
-        # The conversation shards never exchange data; the only collectives are
-        # the timing barrier and a max over two scalars, so gloo (host) is used
-        # and NCCL stays off the data path.
+        # conversation shards never exchange data: gloo carries the work queue, the timing
+        # barrier and a max over two scalars; NCCL stays off the data path.
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    from paper_2506_15556_b200 import B200LM, summarize_percentiles
+    from paper_2506_15556_b200 import B200LM, run_conversation, specstream, summarize_percentiles
     from paper_2506_15556_b200.shapes import SHAPES
-    from paper_2506_15556_b200.workload import WorkloadSpec, c5_config, shard, simulate, synthetic_conversations
+    from paper_2506_15556_b200.simulate import ConversationQueue
+    from paper_2506_15556_b200.workload import WorkloadSpec, c5_config, synthetic_conversations
 
     shape = SHAPES[args.shape]
-    lm = B200LM(shape, seed=0, cost_mode="measured", device=local, max_seq=2048)
+    lm = B200LM(shape, seed=0, cost_mode="modeled", device=local, max_seq=2048)
     spec = WorkloadSpec()
     convs = synthetic_conversations(lm.vocab, spec)
     cfg = c5_config(lm.vocab, spec)
-    mine = shard(convs, rank, world)
     per = args.conv_per_step
-    need = (args.warmup + args.steps) * per
-    if need > len(mine):
-        mine = (mine * (need // max(1, len(mine)) + 1))[:need]
+    live_sched: dict = {}
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
+    def run_step(s: int):
+        first = (s * per * world) % len(convs)
+        q = ConversationQueue(per * world, world, tag=f"step{s}")
+        n = 0
+        while (j := q.claim()) is not None:
+            conv = convs[(first + j) % len(convs)]
+            lm.schedule = []
+            run_conversation(conv.turns, cfg, lm, conversation_id=conv.id)
+            live_sched[conv.id] = summarize_schedule(lm.schedule)
+            n += 1
+        lm.schedule = None
+        return n
+
     for w in range(args.warmup):
-        simulate(mine[w * per:(w + 1) * per], cfg, lm)
+        run_step(w)
     s0 = lm.stats()
-    lm.verify_ms.clear()
-    lm.decode_ms.clear()
     sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
     sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    records, results = [], []
-    base = args.warmup * per
+    done = 0
+    timed = set()
     for k in range(args.steps):
-        r, res = simulate(mine[base + k * per: base + (k + 1) * per], cfg, lm)
-        records += r
-        results += res
+        before = set(live_sched)
+        done += run_step(args.warmup + k)
+        timed |= set(live_sched) - before
     torch.cuda.synchronize()
     ev1.record()
     torch.cuda.synchronize()
@@ -272,31 +355,80 @@ def main():
     elapsed_ms = ev0.elapsed_time(ev1)
     s1 = lm.stats()
     device_ms = s1["gpu_ms"] - s0["gpu_ms"]
-    launches = s1["launches"] - s0["launches"]
-    h2d = s1["h2d_bytes"] - s0["h2d_bytes"]
-    d2h = s1["d2h_bytes"] - s0["d2h_bytes"]
-    decode_rows = s1["decode_steps"] - s0["decode_steps"]
-    all_rows = s1["rows"] - s0["rows"]
-    n_conv = args.steps * per
-    ttfs = summarize_percentiles(records)
-    verify_nonzero = [x for x in lm.verify_ms if x > 0]
-    vals = {"elapsed": elapsed_ms, "device": device_ms}
+    delta = {k: s1[k] - s0[k] for k in ("launches", "h2d_bytes", "d2h_bytes", "decode_steps", "rows", "passes")}
+    vals = {"elapsed": elapsed_ms, "device": device_ms, "done": float(done)}
+    mine = {c: live_sched[c] for c in timed}
     if world > 1:
         t = torch.tensor([elapsed_ms, device_ms], dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        vals = {"elapsed": float(t[0]), "device": float(t[1])}
-    # roofline of the dominant kernel class, CUDA events around every launch
-    prof = lm.profile_decode(steps=8)
-    dom = max(("gate_up_gemm", "down_gemm", "qkv_gemm", "o_gemm", "lm_head", "whole_pass"),
-              key=lambda c: prof[c]["ms"])
-    peaks = {}
+        n = torch.tensor([float(done)], dtype=torch.float64)
+        torch.distributed.all_reduce(n, op=torch.distributed.ReduceOp.SUM)
+        vals = {"elapsed": float(t[0]), "device": float(t[1]), "done": float(n[0])}
+        parts = [None] * world
+        torch.distributed.all_gather_object(parts, mine)
+        mine = {k: v for p in parts for k, v in p.items()}
+    n_conv = int(vals["done"])
+
+    # schedule check against the committed one (what the reference arm prices)
+    committed = load_schedule(shape.name)["conversations"]
+    matched = sum(1 for c, v in mine.items() if committed.get(c) == v)
+    sched_info = {"timed_conversations": len(mine), "match_committed": matched,
+                  "passes_per_conversation": sum(v[0] for v in mine.values()) / max(1, len(mine)),
+                  "rows_per_conversation": sum(v[1] for v in mine.values()) / max(1, len(mine)),
+                  "decode_passes_per_conversation": sum(v[2] for v in mine.values()) / max(1, len(mine))}
+
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
     try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-        hbm, src = float(peaks["hbm_gbs"]), "measured"
+        hbm, src = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "MEASURED_PEAKS.json"
     except (OSError, KeyError, ValueError):
-        hbm, src = 6650.0, "fallback"
+        pass
+    weight_bytes = s1["weight_bytes"]
+    floor_ms = weight_bytes / (hbm * 1e9) * 1e3
+
+    line = {
+        "metric": METRIC, "value": n_conv / (vals["device"] / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": vals["elapsed"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if shape.mode == 1 else "f32",
+        "data": "synthetic (random-init weights, synthetic vocabulary and conversations)",
+        "config": workload_config(args, world),
+        "e2e": {"value": n_conv / (vals["elapsed"] / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": delta["h2d_bytes"] / args.steps,
+                "d2h_bytes_per_step": delta["d2h_bytes"] / args.steps},
+        "schedule": sched_info,
+        "gpu_launches": delta["launches"], "passes": delta["passes"], "rows_computed": delta["rows"],
+        "clocks": clocks,
+    }
+
+    # -- phase 2: measured-cost latency (rank 0) ------------------------------------------
+    if rank == 0 and not args.no_latency:
+        lm.cost_mode = "measured"
+        lm.decode_ms.clear()
+        results = []
+        for i in TTFS_CONVERSATIONS:
+            conv = convs[i % len(convs)]
+            results += run_conversation(conv.turns, cfg, lm, conversation_id=conv.id)
+        records = [specstream.compute_metrics(r.events) for r in results]
+        verify = [e.payload["cost_ms"] for r in results for e in r.events
+                  if e.kind == "verify" and e.payload["cost_ms"] > 0]
+        ttfs = summarize_percentiles(records)
+        line["verify_step_ms"] = {"p50": statistics.median(verify) if verify else None, "count": len(verify),
+                                  "hbm_floor_ms": floor_ms,
+                                  "roofline_frac": floor_ms / statistics.median(verify) if verify else None}
+        line["decode_step_ms"] = {"p50": statistics.median(lm.decode_ms) if lm.decode_ms else None,
+                                  "count": len(lm.decode_ms), "hbm_floor_ms": floor_ms,
+                                  "roofline_frac": floor_ms / statistics.median(lm.decode_ms)
+                                  if lm.decode_ms else None}
+        line["ttfs_ms"] = {**{k: v for k, v in ttfs.items() if "ttfs" in k or "nfetfs" in k},
+                           **ttfs_roofline(results, floor_ms), "turns": len(records),
+                           "conversations": [TTFS_CONVERSATIONS.start, TTFS_CONVERSATIONS.stop - 1],
+                           "cost": "measured (CUDA-event ms of every pass)"}
+        lm.cost_mode = "modeled"
+
+    # -- roofline of the dominant kernel: the decode megakernel pass --------------------------
+    prof = lm.profile_decode(steps=8)
+    dom = max(prof, key=lambda c: prof[c]["ms"])
     dom_gbs = prof[dom]["bytes"] / (prof[dom]["ms"] * 1e-3) / 1e9
-    step_ms = statistics.median(lm.decode_ms) if lm.decode_ms else None
     traffic = None
     ncu_file = ROOT / "profiles" / "ncu_summary.json"
     if ncu_file.exists():
@@ -304,50 +436,24 @@ def main():
             traffic = json.loads(ncu_file.read_text()).get(dom, {}).get("dram_bytes_per_launch_class")
         except ValueError:
             traffic = None
-    line = {
-        "metric": METRIC, "value": world * n_conv / (vals["device"] / 1e3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": vals["elapsed"] / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16" if shape.mode == 1 else "f32",
-        "data": "synthetic (random-init weights, synthetic vocabulary and conversations)",
-        "config": {"workload": "c5: synthetic MT-Bench/Lmsys-length conversations, Llama-3-8B shape, bf16, "
-                               "measured-cost SimClock", "shape": shape.name, "conversations_per_rank_per_step": per,
-                   "chunk_words": cfg.chunk_words, "max_response_tokens": cfg.max_response_tokens,
-                   "l2": "inputs larger than L2 (15 GB of weights streamed per pass)",
-                   "parallelism": f"{world} independent conversation shards (no per-pass collective)"},
-        "e2e": {"value": world * n_conv / (vals["elapsed"] / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps},
-        "verify_step_ms": {"p50": statistics.median(verify_nonzero) if verify_nonzero else None,
-                           "count": len(verify_nonzero),
-                           # a verify window streams the same weights once: same HBM floor
-                           "hbm_floor_ms": lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3,
-                           "roofline_frac": (lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3
-                                             / statistics.median(verify_nonzero)) if verify_nonzero else None},
-        "decode_step_ms": {"p50": step_ms, "count": len(lm.decode_ms),
-                           "hbm_floor_ms": lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3},
-        "ttfs_ms": {**{k: v for k, v in ttfs.items() if "ttfs" in k or "nfetfs" in k},
-                    **ttfs_roofline(results, lm.stats()["weight_bytes"] / (hbm * 1e9) * 1e3)},
-        "turns": len(records),
-        "roofline": {"bound": "hbm",
-                     "kernel": ("mega_kernel: whole 1-row decode pass, one persistent tcgen05 kernel" if dom == "whole_pass"
-                                else f"{dom} (tcgen05 weight-streaming GEMM, 1-row decode step)"),
-                     "achieved": dom_gbs, "peak": hbm, "unit": "GB/s", "frac": dom_gbs / hbm, "traffic": traffic,
-                     "peak_source": src, "per_class_ms": {k: v["ms"] for k, v in prof.items()},
-                     "decode_step_frac": (lm.stats()["weight_bytes"] / (step_ms * 1e-3) / 1e9 / hbm)
-                     if step_ms else None},
-        "gpu_launches": launches, "rows_computed": all_rows, "decode_steps": decode_rows,
-        "clocks": clocks,
-    }
+    line["roofline"] = {"bound": "hbm",
+                        "kernel": ("mega_kernel<decode>: one persistent tcgen05 kernel per 1-row pass"
+                                   if dom == "whole_pass" else dom),
+                        "achieved": dom_gbs, "peak": hbm, "unit": "GB/s", "frac": dom_gbs / hbm,
+                        "traffic": traffic, "peak_source": src, "bytes_per_launch": prof[dom]["bytes"],
+                        "ms_per_launch": prof[dom]["ms"]}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mix = {"decode_rows": decode_rows / n_conv, "extend_rows": (all_rows - decode_rows) / n_conv}
-        t = cpu_port_timing(shape, args.cpu_sample_s, os.cpu_count() or 1)
-        rate = conv_rate_from_passes(t, mix)
+        model = cpu_pass_model(shape, args.cpu_sample_s, os.cpu_count() or 1)
+        cpu_ms = cpu_schedule_ms(model, list(mine.values()))
         line["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": t["threads"], "kind": "port",
-            "sample": (f"oracle decoder (numpy fp32) at {shape.name}: {t['decode_samples']} decode + "
-                       f"{t['verify_samples']} 72-row passes over a 128-token context (median "
-                       f"{t['decode_ms']:.0f} / {t['verify_ms']:.0f} ms), scaled by this run's pass mix "
-                       f"{ {k: round(v, 1) for k, v in mix.items()} } per conversation"),
+            "value": len(mine) / (cpu_ms / 1e3), "unit": UNIT, "cores": model["threads"], "kind": "port",
+            "sample": (f"oracle decoder (numpy fp32, {cpu_model()}) at {shape.name}: decode pass "
+                       f"{model['decode_ms']:.1f} ms, wider passes {model['a_ms']:.1f} ms + "
+                       f"{model['b_ms_per_row']:.2f} ms/row; {sum(model['samples'].values())} sampled passes of "
+                       f"1/8/32/72 rows over a 128-token context, "
+                       f"summed over this run's pass schedule ({len(mine)} conversations)"),
+            "per_pass_ms": model["median_ms"],
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -4,14 +4,26 @@ CPU restatements used only as the checker by tests/, `__graft_entry__.smoke()`
 and the `cpu_baseline` / `--impl reference` legs of bench.py:
 
 * `weights`  — the counter-based weight generator (bit-identical to csrc/init.cu)
-* `decoder`  — float64 numpy decoder + `CpuDecoderLM`, the `LanguageModel`
-               contract of `/root/reference/pkg/src/specstream/lm.py:182-203`
-* `ngram`    — the reference's `NGramLM` (lm.py:216-243), pinned by its golden
-               sequence (test_lm.py:161-168)
-* `lm_surface` — value types of lm.py:32-154 so the oracle runs without the
-               reference installed
+* `decoder`  — float64 numpy decoder + `CpuDecoderLM`, a reference
+               `LanguageModel` (`/root/reference/pkg/src/specstream/lm.py:157-213`)
 
-Decoder numerics are parity-unpinned by the reference (it has no decoder); the
-algorithm layer is pinned by golden event logs the reference itself produced
-(tests/golden/make_golden.py).
+The algorithm layer is the reference's own package (`specstream`, installed
+into baseline/_ref by tools/install_reference.sh), so the oracle has no copy
+of it. Decoder numerics are parity-unpinned by the reference (it has no
+decoder); the algorithm layer is pinned by golden event logs the reference
+itself produced (tests/golden/make_golden.py).
 """
+
+from __future__ import annotations
+
+import importlib
+import sys
+from pathlib import Path
+
+_REF = Path(__file__).resolve().parent.parent / "baseline" / "_ref"
+try:
+    specstream = importlib.import_module("specstream")
+except ImportError:
+    if str(_REF) not in sys.path:
+        sys.path.append(str(_REF))
+    specstream = importlib.import_module("specstream")

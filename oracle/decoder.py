@@ -30,8 +30,11 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import specstream
 from . import weights as W
-from .lm_surface import CacheHandle, LatencyModel, LogitsBlock, PrefixViolationError, fresh_backend_id
+
+_lm = specstream.lm
+CacheHandle, LogitsBlock, PrefixViolationError = _lm.CacheHandle, _lm.LogitsBlock, _lm.PrefixViolationError
 
 MODE_F32 = 0
 MODE_BF16 = 1
@@ -214,19 +217,16 @@ def top2_gap(row: np.ndarray) -> float:
     return float(part[1] - part[0])
 
 
-class CpuDecoderLM:
-    """Duck-typed `LanguageModel` (`lm.py:157-213`) over `DecoderOracle`.
+class CpuDecoderLM(_lm.LanguageModel):
+    """A reference `LanguageModel` (`lm.py:157-213`) over `DecoderOracle`.
 
     Rows for already-resident positions are kept from the pass that computed
     them (float64 accumulation makes recomputation immaterial), so `forward`
     costs only the uncached tail, like the B200 backend.
     """
 
-    def __init__(self, shape: dict, vocab, seed: int = 0, latency: LatencyModel | None = None,
-                 dtype=np.float64):
-        self.vocab = vocab
-        self.latency = latency or LatencyModel()
-        self._backend_id = fresh_backend_id()
+    def __init__(self, shape: dict, vocab, seed: int = 0, latency=None, dtype=np.float64):
+        super().__init__(vocab, latency)
         self.model = DecoderOracle(shape, seed, dtype=dtype)
         self._rows: list[np.ndarray] = []  # logits row per resident position
         self.min_gap = np.inf  # smallest top-2 gap over every row handed out
@@ -234,14 +234,6 @@ class CpuDecoderLM:
 
     def _record_gap(self, gap: float) -> None:
         self.min_gap = min(self.min_gap, gap)
-
-    @property
-    def vocab_size(self) -> int:
-        return self.model.V
-
-    @property
-    def eos_id(self) -> int:
-        return 0
 
     def _materialize(self, context: list[int]) -> None:
         m = self.model
@@ -273,9 +265,8 @@ class CpuDecoderLM:
         the formatted judge prompt (lm.py:117-131), then the last row's scores of
         "yes" and "no" (lm.py:107-114). Judge text is mapped to ids by the
         vocabulary's `judge_ids` (host tokenisation, identical on both sides)."""
-        from .lm_surface import JUDGE_TEMPLATE, JudgeResult
         ids = self.vocab.judge_ids
-        toks = ids(JUDGE_TEMPLATE.format(partial_prompt=partial_prompt, partial_answer=partial_answer))
+        toks = ids(_lm.format_judge_prompt(partial_prompt, partial_answer))
         block, _, cost = self.forward(toks)
         row = block.last_row
-        return JudgeResult(yes_score=float(row[ids("yes")[0]]), no_score=float(row[ids("no")[0]])), cost
+        return _lm.JudgeResult(yes_score=float(row[ids("yes")[0]]), no_score=float(row[ids("no")[0]])), cost

@@ -124,7 +124,9 @@ def last_error(lib) -> str:
 def check(lib, rc: int, what: str = "") -> None:
     if rc == PS_OK:
         return
-    from .model_api import PrefixViolationError  # local import: avoid a cycle at module load
+    from ._specstream import specstream  # local import: the ABI check needs no reference
+
+    PrefixViolationError = specstream.lm.PrefixViolationError
     msg = f"{what}: {last_error(lib)}" if what else last_error(lib)
     if rc == PS_ERR_PREFIX:
         raise PrefixViolationError(msg)

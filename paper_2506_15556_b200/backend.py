@@ -1,10 +1,9 @@
 """`B200LM`: the reference's `LanguageModel` surface backed by the CUDA runtime.
 
-Drop-in for `specstream.lm.LanguageModel` (`/root/reference/pkg/src/specstream/
-lm.py:157-213`): the reference's own `verify_greedy`, `ar_generate`,
-`greedy_decode` and `run_turn` run on it unchanged (tests/test_dropin_gpu.py),
-and this package's algorithm layer additionally uses the fused entry points
-`verify_greedy_fused` / `decode_greedy_fused` / `discard_after`.
+A subclass of `specstream.lm.LanguageModel` (`/root/reference/pkg/src/specstream/
+lm.py:157-213`), so the reference's own `verify_greedy`, `verify_topk`,
+`verify_reflection`, `ar_generate`, `jacobi_generate`, `greedy_decode`,
+`run_turn` and `run_baseline` run on it unchanged (tests/test_gpu_dropin.py).
 
 Semantics kept from the reference:
 
@@ -13,16 +12,23 @@ Semantics kept from the reference:
   cost. Handle checks raise `PrefixViolationError` (`lm.py:192-199`).
 * cache transparency (`SPEC.md:158`): rows are bit-identical whatever the
   cache, because the device keeps one resident sequence, reuses its longest
-  common prefix, and every kernel is batch-invariant (csrc/layers.cu).
+  common prefix, and every kernel is batch-invariant. A
+  `_prefill` over a prefix the verify pass left resident costs nothing, and
+  the first decode after a verify reads the correction token the verify pass
+  already scored.
 
 Cost modes: "modeled" charges the reference's `LatencyModel` exactly
 (`lm.py:56-57`), so decisions and event logs are comparable bit-for-bit with
 the CPU oracle; "measured" charges the CUDA-event milliseconds of the work
-the device actually did (a prefix hit costs ~0).
+the device actually did (a prefix hit costs 0).
 
 Rows are lazy: a `LazyRow` knows its argmax (computed on the device by the
-fused LM-head kernel) and materialises the fp32 logits only when something
-other than `np.argmax` touches it.
+LM-head phase) and materialises the fp32 logits only when something other
+than `np.argmax` touches it.
+
+Fused entry points (`verify_greedy_fused`, `verify_topk_fused`,
+`decode_greedy_fused`) bind the one-call C-ABI paths; `fused.py` plugs the
+verify ones into the reference's loop.
 """
 
 from __future__ import annotations
@@ -33,10 +39,54 @@ import math
 import numpy as np
 
 from . import _native
-from .model_api import (CacheHandle, JudgeUnsupportedError, LanguageModel, LatencyModel, LogitsBlock,
-                        PrefixViolationError, decoder_judge)
+from ._specstream import specstream
 from .shapes import MODE_BF16, DecoderShape
 from .vocab import SyntheticVocabulary, terminator_mask
+
+_lm = specstream.lm
+CacheHandle = _lm.CacheHandle
+LogitsBlock = _lm.LogitsBlock
+LatencyModel = _lm.LatencyModel
+JudgeResult = _lm.JudgeResult
+JudgeUnsupportedError = _lm.JudgeUnsupportedError
+PrefixViolationError = _lm.PrefixViolationError
+
+
+def decoder_judge(lm, partial_prompt: str, partial_answer: str):
+    """PredGen's self-consistency judge for a decoder backend: one fresh pass
+    over the reference's formatted judge prompt (`format_judge_prompt`,
+    lm.py:117-131), then the exact last row's scores of "yes" and "no"
+    (`JudgeResult.consistent` iff yes > no, lm.py:107-114). Returns
+    (JudgeResult, cost of the pass)."""
+    ids = lm.vocab.judge_ids
+    toks = ids(_lm.format_judge_prompt(partial_prompt, partial_answer))
+    block, _, cost = lm.forward(toks)
+    row = block.last_row
+    yes, no = ids("yes")[0], ids("no")[0]
+    return JudgeResult(yes_score=float(row[yes]), no_score=float(row[no])), cost
+
+
+def ps_config(shape: DecoderShape, seed: int = 0, max_seq: int = 2048, device: int = 0, vocab_shards: int = 1,
+              shard_rank: int = 0, use_graphs: bool = True) -> _native.PsConfig:
+    """The `ps_config` (include/predgen_b200.h) of a decoder shape: the logit biases
+    of the terminator / EOS ids are given in units of the logit std 0.02*sqrt(H)."""
+    cfg = _native.PsConfig()
+    sigma = 0.02 * math.sqrt(shape.hidden)
+    for name in ("vocab", "hidden", "layers", "heads", "kv_heads", "head_dim", "intermediate", "mode"):
+        setattr(cfg, name, int(getattr(shape, name)))
+    cfg.tied_embeddings = int(shape.tied_embeddings)
+    cfg.qkv_bias = int(shape.qkv_bias)
+    cfg.rope_theta = shape.rope_theta
+    cfg.rms_eps = shape.rms_eps
+    cfg.term_bias = float(np.float32(shape.term_bias_sigma * sigma))
+    cfg.eos_bias = float(np.float32(shape.eos_bias_sigma * sigma))
+    cfg.seed = seed
+    cfg.max_seq = max_seq
+    cfg.device = device
+    cfg.vocab_shards = vocab_shards
+    cfg.shard_rank = shard_rank
+    cfg.use_graphs = int(use_graphs)
+    return cfg
 
 
 class LazyRow:
@@ -97,7 +147,7 @@ class _LazyRows:
         return arr if dtype is None else arr.astype(dtype)
 
 
-class B200LM(LanguageModel):
+class B200LM(_lm.LanguageModel):
     def __init__(self, shape: DecoderShape, vocab=None, seed: int = 0, latency: LatencyModel | None = None,
                  cost_mode: str = "modeled", device: int = 0, max_seq: int = 2048, use_graphs: bool = True,
                  vocab_shards: int = 1, shard_rank: int = 0) -> None:
@@ -111,22 +161,8 @@ class B200LM(LanguageModel):
         self.cost_mode = cost_mode
         self._lib = _native.load()
         self._h = ctypes.c_void_p()
-        cfg = _native.PsConfig()
-        sigma = 0.02 * math.sqrt(shape.hidden)
-        for name in ("vocab", "hidden", "layers", "heads", "kv_heads", "head_dim", "intermediate", "mode"):
-            setattr(cfg, name, int(getattr(shape, name)))
-        cfg.tied_embeddings = int(shape.tied_embeddings)
-        cfg.qkv_bias = int(shape.qkv_bias)
-        cfg.rope_theta = shape.rope_theta
-        cfg.rms_eps = shape.rms_eps
-        cfg.term_bias = float(np.float32(shape.term_bias_sigma * sigma))
-        cfg.eos_bias = float(np.float32(shape.eos_bias_sigma * sigma))
-        cfg.seed = seed
-        cfg.max_seq = max_seq
-        cfg.device = device
-        cfg.vocab_shards = vocab_shards
-        cfg.shard_rank = shard_rank
-        cfg.use_graphs = int(use_graphs)
+        cfg = ps_config(shape, seed, max_seq=max_seq, device=device, vocab_shards=vocab_shards,
+                        shard_rank=shard_rank, use_graphs=use_graphs)
         self.seed = seed
         self.max_seq = max_seq
         self.vocab_shards = vocab_shards
@@ -135,10 +171,12 @@ class B200LM(LanguageModel):
         mask = terminator_mask(vocab)
         buf = (ctypes.c_uint8 * len(mask)).from_buffer_copy(mask)
         self._call("ps_set_terminators", buf, len(mask))
-        self._step_ms = None  # EMA of measured decode-step time
         self.last_verify_ms = 0.0
         self.verify_ms: list[float] = []
-        self.decode_ms: list[float] = []
+        self.decode_ms: list[float] = []   # device ms of every 1-row pass
+        self.extend_ms: list[tuple] = []   # (rows, device ms) of every wider pass
+        # (context length, rows computed) of every pass, when a caller sets it to a list
+        self.schedule: list | None = None
 
     # -- plumbing -----------------------------------------------------------------
     def _call(self, name: str, *args) -> None:
@@ -161,6 +199,17 @@ class B200LM(LanguageModel):
         st = _native.PsStats()
         self._call("ps_get_stats", ctypes.byref(st))
         return st.as_dict()
+
+    def _rows_computed(self) -> int:
+        st = _native.PsStats()
+        self._call("ps_get_stats", ctypes.byref(st))
+        return int(st.rows)
+
+    def _note_verify_pass(self, n_ctx: int, rows_before: int) -> None:
+        if self.schedule is not None:
+            rows = self._rows_computed() - rows_before
+            if rows:
+                self.schedule.append((n_ctx, rows))
 
     def resident(self) -> list[int]:
         n = ctypes.c_int32()
@@ -215,10 +264,29 @@ class B200LM(LanguageModel):
         return list(am[: n - row_from]), computed.value, ms.value
 
     # -- LanguageModel surface ---------------------------------------------------------
+    def _cached_start(self, context, cache) -> int:
+        """The reference's handle rules (lm.py:190-199); the first uncached position."""
+        start = 0
+        if cache is not None:
+            if cache.backend_id != self._backend_id:
+                raise PrefixViolationError("cache handle belongs to a different backend instance")
+            if tuple(context[: len(cache.prefix)]) != tuple(cache.prefix):
+                raise PrefixViolationError("context does not extend the cached prefix")
+            start = len(cache.prefix)
+        if start >= len(context):
+            raise PrefixViolationError("forward pass requires at least one uncached position")
+        return start
+
     def forward(self, context, cache=None):
         start = self._cached_start(context, cache)
         ctx = tuple(int(t) for t in context)
-        argmax, _, ms = self._sync(list(ctx), start)
+        argmax, computed, ms = self._sync(list(ctx), start)
+        if computed and self.schedule is not None:
+            self.schedule.append((len(ctx), computed))
+        if computed == 1:
+            self.decode_ms.append(ms)
+        elif computed > 1:
+            self.extend_ms.append((computed, ms))
         rows = _LazyRows(self, ctx, start, argmax)
         return LogitsBlock(rows, start), CacheHandle(ctx, self._backend_id), self._cost(len(ctx) - start, ms)
 
@@ -229,7 +297,7 @@ class B200LM(LanguageModel):
             raise JudgeUnsupportedError("the judge needs the full LM-head row (vocab-sharded instance)")
         return decoder_judge(self, partial_prompt, partial_answer)
 
-    # -- fused fast paths (used by this package's verifier / generator) ------------------
+    # -- fused one-call paths (C-ABI; fused.py plugs the verifiers into the loop) -------
     def verify_greedy_fused(self, prompt, candidate):
         """One fused pass: (k, handle over prompt ++ candidate, cost)."""
         if not prompt:
@@ -239,8 +307,10 @@ class B200LM(LanguageModel):
         k = ctypes.c_int32()
         term = ctypes.c_int32()
         ms = ctypes.c_float()
+        rows0 = self._rows_computed() if self.schedule is not None else 0
         self._call("ps_verify_greedy", p, len(prompt), c, len(candidate), ctypes.byref(k), ctypes.byref(term),
                    None, ctypes.byref(ms))
+        self._note_verify_pass(len(prompt) + len(candidate), rows0)
         self.last_verify_ms = ms.value
         self.verify_ms.append(ms.value)
         seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)
@@ -260,7 +330,9 @@ class B200LM(LanguageModel):
         """Fused top-k verify (rank counting on the device): (k, handle over prompt ++ candidate, cost)."""
         if not prompt:
             raise ValueError("verification requires a nonempty prompt context")
+        rows0 = self._rows_computed() if self.schedule is not None else 0
         d = self.verify_topk_detail(prompt, candidate, topk)
+        self._note_verify_pass(len(prompt) + len(candidate), rows0)
         self.last_verify_ms = d["gpu_ms"]
         self.verify_ms.append(d["gpu_ms"])
         seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)
@@ -279,7 +351,10 @@ class B200LM(LanguageModel):
                 "gpu_ms": ms.value}
 
     def decode_greedy_fused(self, seq, n: int):
-        """Up to n greedy tokens continuing `seq` (stops after EOS): [(token, cost_ms)]."""
+        """Up to n greedy tokens continuing `seq`, stopping after EOS: [(token, cost_ms)].
+        One C-ABI call: the first token is the resident row's argmax, the rest are
+        graph-replayed 1-row steps chained on the device (no host round trip per token).
+        Same tokens as the reference's `greedy_decode` (lm.py:350-382)."""
         if n <= 0:
             return []
         s = _native.i32_array(seq)
@@ -293,19 +368,11 @@ class B200LM(LanguageModel):
             steps.append((int(out[i]), cost))
             if i > 0 or ms[i] > 0:
                 self.decode_ms.append(ms[i])
-        if got.value > 1:
-            tail = [ms[i] for i in range(1, got.value)]
-            avg = sum(tail) / len(tail)
-            self._step_ms = avg if self._step_ms is None else 0.8 * self._step_ms + 0.2 * avg
         return steps
 
-    def discard_after(self, n: int) -> None:
+    def truncate(self, n: int) -> None:
+        """Roll the resident sequence back to n tokens (ps_truncate)."""
         self._call("ps_truncate", int(n))
-
-    def decode_cost_estimate(self) -> float:
-        if self.cost_mode == "modeled":
-            return self.latency.pass_cost(1)
-        return self._step_ms if self._step_ms is not None else 1.0
 
     def profile_decode(self, steps: int = 4) -> dict:
         ms = (ctypes.c_double * 8)()

@@ -1,21 +1,28 @@
-"""Sharded conversation simulation with JSONL event logs (SURVEY.md §8f row 4).
+"""Sharded conversation simulation with JSONL event logs (SURVEY.md §8e, §8f row 4).
 
 The multi-GPU form of the reference's `simulate` command (cli.py:92-106 ->
-metrics.py:202-216 `run_dataset`; event files as pipeline.py:108-130
-`write_events_jsonl`). One process per GPU; conversation i runs on rank
-i mod G with that rank's own backend; every turn's events go to
-`<out>/events/<conversation>_<round>.jsonl`; rank 0 gathers the per-turn
-metrics (a torch.distributed object gather, host side only — no data-path
-collective) and writes them in dataset order to `<out>/metrics.jsonl` plus a
-`<out>/summary.json` with means and percentiles.
+metrics.py:202-216 `run_dataset`, a sequential loop over conversations that
+share one backend). Conversations are independent units, so:
+
+* one process per GPU, each with its own `B200LM` replica; no per-pass
+  collective;
+* a dynamic work queue: ranks claim the next conversation index with an
+  atomic `add` on the torch.distributed store (`ConversationQueue`), so
+  lognormal-length conversations balance across ranks instead of a static
+  i mod G split;
+* every turn's events go to `<out>/events/<conversation>_<round>.jsonl`
+  (the reference's `write_events_jsonl`, pipeline.py:108-130); rank 0
+  gathers the per-turn metrics (a host-side object gather) and writes them in
+  dataset order to `<out>/metrics.jsonl` plus `<out>/summary.json`.
 
 In modeled-cost mode (`B200LM(cost_mode="modeled")`, the reference's
-LatencyModel) a pass's cost depends only on the caller's cache handle, never
-on what else ran on the device, so every output file is byte-identical for
-any G — the analogue of the reference's determinism criterion
-(test_acceptance.py:231-255), checked by tests/test_simulate.py at G = 1, 2.
+LatencyModel) a pass's cost depends only on the caller's cache handle and the
+kernels are batch-invariant, so a conversation's events do not depend on
+which rank ran it or what ran before it: every output file is byte-identical
+for any G and any claim order — the analogue of the reference's determinism
+criterion (test_acceptance.py:231-255).
 
-    python -m torch.distributed.run --nproc-per-node G --master-addr 127.0.0.1 \
+    python -m torch.distributed.run --nproc-per-node G --master-addr 127.0.0.1 \\
         -m paper_2506_15556_b200.simulate --synthetic 64 --shape llama-3-8b --out runs/x
 """
 
@@ -23,27 +30,54 @@ from __future__ import annotations
 
 import argparse
 import dataclasses
+import itertools
 import json
 import os
 from pathlib import Path
 
-from .turn import run_conversation, write_events_jsonl
-from .turn_metrics import compute_metrics, load_dataset, summarize, summarize_percentiles
+from ._specstream import specstream
+from .fused import run_conversation
+from .report import summarize_percentiles
+
+_queue_ids = itertools.count()
+
+
+class ConversationQueue:
+    """Work queue over indices [0, n): `claim()` returns the next unclaimed index or None.
+
+    world == 1: a local counter. world > 1: an atomic counter on the process
+    group's TCPStore (one round trip per claim, ~50 µs, against seconds of
+    device work per conversation)."""
+
+    def __init__(self, n: int, world: int = 1, store=None, tag: str | None = None):
+        self.n = n
+        self._local = itertools.count()
+        self._store = None
+        if world > 1:
+            import torch.distributed as dist
+
+            base = store if store is not None else dist.distributed_c10d._get_default_store()
+            # a fresh key per queue (every rank constructs its queues in the same order)
+            self._store = dist.PrefixStore(f"ps_queue/{tag if tag is not None else next(_queue_ids)}", base)
+
+    def claim(self):
+        i = self._store.add("next", 1) - 1 if self._store is not None else next(self._local)
+        return i if i < self.n else None
 
 
 def run_sharded(conversations, cfg, lm, out_dir, rank: int = 0, world: int = 1, baseline: bool = False,
-                group=None) -> list[dict]:
-    """Simulate this rank's shard, write its event logs; rank 0 writes the report.
+                group=None, queue: ConversationQueue | None = None) -> list[dict]:
+    """Simulate the conversations this rank claims, write their event logs; rank 0 writes the report.
 
     Returns the per-turn metrics (all ranks' on rank 0, this rank's elsewhere)."""
     out = Path(out_dir)
+    queue = queue if queue is not None else ConversationQueue(len(conversations), world)
     recs = []
-    for i, conv in enumerate(conversations):
-        if i % world != rank:
-            continue
+    while (i := queue.claim()) is not None:
+        conv = conversations[i]
         for res in run_conversation(conv.turns, cfg, lm, conversation_id=conv.id, baseline=baseline):
-            m = compute_metrics(res.events)
-            write_events_jsonl(res.events, out / "events" / f"{conv.id}_{m.round}.jsonl")
+            m = specstream.compute_metrics(res.events)
+            specstream.write_events_jsonl(res.events, out / "events" / f"{conv.id}_{m.round}.jsonl")
             recs.append((i, dataclasses.asdict(m)))
     if world > 1:
         import torch.distributed as dist
@@ -54,15 +88,14 @@ def run_sharded(conversations, cfg, lm, out_dir, rank: int = 0, world: int = 1, 
     recs.sort(key=lambda x: (x[0], x[1]["round"]))
     rows = [r for _, r in recs]
     if rank == 0:
+        out.mkdir(parents=True, exist_ok=True)
         with (out / "metrics.jsonl").open("w") as fh:
             for r in rows:
                 fh.write(json.dumps(r, sort_keys=True) + "\n")
-        from .turn_metrics import MetricsRecord
-
-        records = [MetricsRecord(**r) for r in rows]
+        records = [specstream.MetricsRecord(**r) for r in rows]
         # nothing here depends on G (reports must be identical for any world size)
         summary = {"turns": len(rows), "conversations": len(conversations), "baseline": baseline,
-                   "mean": summarize(records), "percentiles": summarize_percentiles(records)}
+                   "mean": specstream.summarize(records), "percentiles": summarize_percentiles(records)}
         (out / "summary.json").write_text(json.dumps(summary, indent=2, sort_keys=True) + "\n")
     return rows
 
@@ -80,6 +113,8 @@ def main(argv=None) -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PS_SHARE_GPU") == "1":
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
@@ -92,7 +127,7 @@ def main(argv=None) -> int:
     shape = SHAPES[a.shape]
     vocab = SyntheticVocabulary(shape.vocab)
     spec = WorkloadSpec(conversations=a.synthetic, seed=a.seed) if a.synthetic else WorkloadSpec()
-    convs = synthetic_conversations(vocab, spec) if a.synthetic else load_dataset(a.dataset)
+    convs = synthetic_conversations(vocab, spec) if a.synthetic else specstream.load_dataset(a.dataset)
     cfg = c5_config(vocab, spec)
     lm = B200LM(shape, seed=a.seed, device=local, cost_mode=a.cost_mode)
     try:

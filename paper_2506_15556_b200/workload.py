@@ -18,8 +18,12 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .turn import PipelineConfig, run_conversation
-from .turn_metrics import Conversation, compute_metrics
+from ._specstream import specstream
+from .fused import run_conversation
+
+PipelineConfig = specstream.PipelineConfig
+Conversation = specstream.Conversation
+compute_metrics = specstream.compute_metrics
 
 
 @dataclass(frozen=True)

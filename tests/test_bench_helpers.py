@@ -42,8 +42,17 @@ def test_ttfs_roofline_skips_turns_without_a_sentence():
     assert bench.ttfs_roofline([turn(events)], pass_floor_ms=2.0) == {}
 
 
-def test_conversation_rate_from_pass_times():
-    rate = bench.conv_rate_from_passes({"decode_ms": 3.0, "verify_ms": 72.0},
-                                       {"decode_rows": 100, "extend_rows": 144})
-    # 100 * 3 ms + 144 / 72 * 72 ms = 444 ms per conversation
-    assert rate == pytest.approx(1000.0 / 444.0)
+def test_cpu_schedule_pricing():
+    model = {"decode_ms": 50.0, "a_ms": 100.0, "b_ms_per_row": 10.0}
+    sched = [bench.summarize_schedule([(30, 1), (31, 1), (40, 72), (41, 1)])]
+    assert sched[0] == [4, 75, 3, 1]
+    # 3 decode passes * 50 ms + one 72-row pass at 100 ms + 72 * 10 ms
+    assert bench.cpu_schedule_ms(model, sched) == pytest.approx(970.0)
+
+
+def test_both_arms_print_the_same_config():
+    args = bench.parse(["--steps", "5", "--warmup", "3", "--conv-per-step", "2"])
+    cfg = bench.workload_config(args, world=4)
+    assert cfg["timed_conversation_ids"] == [24, 64]
+    assert bench.workload_config(bench.parse(["--impl", "reference", "--steps", "5", "--warmup", "3",
+                                              "--conv-per-step", "2"]), world=4) == cfg

@@ -12,12 +12,11 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN  # noqa: F401
-from paper_2506_15556_b200 import B200LM
-from paper_2506_15556_b200.generation import GenerationBudget, jacobi_generate
-from paper_2506_15556_b200.model_api import greedy_decode
+from paper_2506_15556_b200 import B200LM, greedy_decode, jacobi_generate, specstream
 from paper_2506_15556_b200.shapes import TINY, small_shape
 
 pytestmark = pytest.mark.gpu
+GenerationBudget = specstream.GenerationBudget
 
 
 @pytest.mark.parametrize("shape", [TINY, small_shape()], ids=["f32", "bf16"])

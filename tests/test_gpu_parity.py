@@ -15,9 +15,9 @@ from conftest import GOLDEN
 from oracle import weights as W
 from oracle.decoder import CpuDecoderLM, DecoderOracle, top2_gap
 from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_baseline, run_turn
-from paper_2506_15556_b200.model_api import LatencyModel, PrefixViolationError, greedy_decode
+from paper_2506_15556_b200 import LatencyModel, PrefixViolationError, greedy_decode, specstream
 from paper_2506_15556_b200.shapes import MODE_BF16, MODE_F32, TINY, small_shape
-from paper_2506_15556_b200.vocab import SyntheticVocabulary
+from paper_2506_15556_b200 import SyntheticVocabulary
 
 pytestmark = pytest.mark.gpu
 
@@ -101,10 +101,10 @@ def test_f32_turn_event_logs_match_reference_golden(tiny, i):
 
 
 def _rows_one_pass_vs_stepwise(lm, toks):
-    lm.discard_after(0)
+    lm.truncate(0)
     block, _, _ = lm.forward(toks)
     one = np.stack([np.asarray(block.row_for(p)) for p in range(len(toks))])
-    lm.discard_after(0)
+    lm.truncate(0)
     step = []
     for n in range(1, len(toks) + 1):
         b, _, _ = lm.forward(toks[:n])
@@ -165,17 +165,17 @@ def test_long_context_bitwise_and_decode(small_bf16):
     graph-replayed decode continues with the forward argmax."""
     lm = small_bf16
     toks = rand_tokens(np.random.default_rng(5), lm.vocab_size, 700)
-    lm.discard_after(0)
+    lm.truncate(0)
     block, _, _ = lm.forward(toks)
     one = np.stack([np.asarray(block.row_for(p)) for p in range(690, 700)])
-    lm.discard_after(0)
+    lm.truncate(0)
     lm.forward(toks[:690])
     step = []
     for n in range(691, 701):
         b, _, _ = lm.forward(toks[:n])
         step.append(np.asarray(b.row_for(n - 1)))
     assert np.array_equal(one.view(np.uint32), np.stack(step).view(np.uint32))
-    lm.discard_after(0)
+    lm.truncate(0)
     fused = [t for t, _ in lm.decode_greedy_fused(toks, 6)]
     seq = greedy_decode(lm, toks, max_new=6, stop=None)
     assert seq[len(toks):] == fused[: len(seq) - len(toks)]
@@ -200,7 +200,7 @@ def test_bf16_agreement_with_oracle(small_bf16):
     agree = total = 0
     for trial in range(4):
         toks = rand_tokens(rng, SMALL_BF16.vocab, 64)
-        small_bf16.discard_after(0)
+        small_bf16.truncate(0)
         block, _, _ = small_bf16.forward(toks)
         got = np.stack([np.asarray(block.row_for(p)) for p in range(len(toks))])
         ref.reset()
@@ -232,29 +232,16 @@ def test_bf16_pipeline_lossless(mode):
 
 
 def test_fused_and_generic_paths_agree():
-    """The reference-style generic loop (forward + np.argmax rows) and the fused
-    device paths produce identical event logs in modeled-cost mode."""
-
-    class Generic:
-        def __init__(self, lm):
-            self._lm = lm
-            self.vocab, self.latency, self._backend_id = lm.vocab, lm.latency, lm._backend_id
-
-        eos_id = 0
-
-        def forward(self, context, cache=None):
-            return self._lm.forward(context, cache)
-
-        def judge_consistency(self, a, b):
-            return self._lm.judge_consistency(a, b)
-
+    """The reference's own loop (forward + np.argmax on lazy rows, specstream.run_turn)
+    and the fused verifier binding (paper_2506_15556_b200.run_turn) produce identical
+    event logs in modeled-cost mode."""
     rec = TINY_TURNS["turns"][0]
     cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
     lm = B200LM(TINY, seed=0, max_seq=1024)
     try:
         stream = make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words)
         fused = run_turn([], stream, cfg, lm)
-        generic = run_turn([], stream, cfg, Generic(lm))
+        generic = specstream.run_turn([], stream, cfg, lm)
         assert [e.to_dict() for e in fused.events] == [e.to_dict() for e in generic.events]
     finally:
         lm.close()

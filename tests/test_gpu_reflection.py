@@ -12,9 +12,9 @@ import pytest
 from conftest import GOLDEN  # noqa: F401
 from oracle.decoder import CpuDecoderLM
 from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_turn
-from paper_2506_15556_b200.model_api import LatencyModel
+from paper_2506_15556_b200 import LatencyModel
 from paper_2506_15556_b200.shapes import TINY
-from paper_2506_15556_b200.vocab import SyntheticVocabulary
+from paper_2506_15556_b200 import SyntheticVocabulary
 
 pytestmark = pytest.mark.gpu
 

@@ -15,9 +15,9 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN  # noqa: F401  (conftest registers the marker)
-from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_turn
+from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_turn, specstream
 from paper_2506_15556_b200.shapes import TINY, small_shape
-from paper_2506_15556_b200.verifier import verify_greedy, verify_topk
+from paper_2506_15556_b200.fused import verify_greedy, verify_topk
 
 pytestmark = pytest.mark.gpu
 
@@ -96,23 +96,13 @@ def test_topk_verifier_fused_equals_generic(lm):
 
 
 def test_topk_turn_event_logs_fused_equals_generic():
-    class Generic:
-        def __init__(self, inner):
-            self._lm = inner
-            self.vocab, self.latency, self._backend_id = inner.vocab, inner.latency, inner._backend_id
-
-        eos_id = 0
-
-        def forward(self, context, cache=None):
-            return self._lm.forward(context, cache)
-
     cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32, verifier="topk", topk_k=3)
     lm = B200LM(TINY, seed=0, max_seq=1024)
     try:
         words = " ".join(f"w{int(t)}" for t in np.random.default_rng(5).integers(4, TINY.vocab, 48))
         stream = make_stream(words, cfg.rate_chars_per_min, cfg.chunk_words)
         fused = run_turn([], stream, cfg, lm)
-        generic = run_turn([], stream, cfg, Generic(lm))
+        generic = specstream.run_turn([], stream, cfg, lm)  # the reference's topk_tokens on materialised rows
         assert [e.to_dict() for e in fused.events] == [e.to_dict() for e in generic.events]
     finally:
         lm.close()

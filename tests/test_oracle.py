@@ -1,6 +1,6 @@
 """The CPU oracle itself: weight generator spec, decoder contract, and the
-reference's algorithm layer replayed through this package's loop on the
-oracle decoder (config c1 golden logs, tests/golden/tiny_turns.json)."""
+installed reference's loop on the oracle decoder reproducing the config c1
+golden logs (tests/golden/tiny_turns.json)."""
 
 import json
 
@@ -10,10 +10,10 @@ import pytest
 from conftest import GOLDEN
 from oracle import weights as W
 from oracle.decoder import CpuDecoderLM, DecoderOracle
-from paper_2506_15556_b200 import PipelineConfig, make_stream, run_baseline, run_turn
-from paper_2506_15556_b200.model_api import LatencyModel, PrefixViolationError as PkgPrefix
+from paper_2506_15556_b200 import SyntheticVocabulary, specstream
 from paper_2506_15556_b200.shapes import TINY, small_shape
-from paper_2506_15556_b200.vocab import SyntheticVocabulary
+
+LatencyModel = specstream.LatencyModel
 
 TINY_TURNS = json.loads((GOLDEN / "tiny_turns.json").read_text())
 
@@ -59,19 +59,19 @@ def test_cpu_lm_contract():
     block2, h2, cost2 = lm.forward(ctx + [9], handle)
     assert block2.first_position == 4 and cost2 == LatencyModel().pass_cost(1)
     np.testing.assert_array_equal(block2.rows[0], lm.forward(ctx + [9])[0].rows[4])
-    with pytest.raises(ValueError):
+    with pytest.raises(specstream.PrefixViolationError):
         lm.forward(ctx, h2.truncated(4))
 
 
 @pytest.mark.parametrize("i", range(len(TINY_TURNS["turns"])))
 def test_tiny_turn_replay_matches_reference(i):
-    """Reference algorithm + oracle decoder (golden) == package algorithm + oracle decoder."""
+    """The installed reference + oracle decoder reproduces the golden turn logs."""
     rec = TINY_TURNS["turns"][i]
     vocab = SyntheticVocabulary(TINY.vocab)
-    cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
-    for arm, run in (("speculative", run_turn), ("baseline", run_baseline)):
+    cfg = specstream.PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32)
+    for arm, run in (("speculative", specstream.run_turn), ("baseline", specstream.run_baseline)):
         lm = CpuDecoderLM(TINY_TURNS["shape"], vocab, seed=TINY_TURNS["seed"], latency=LatencyModel())
-        res = run([], make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+        res = run([], specstream.make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
         assert res.final_text == rec[arm]["final_text"]
         assert [e.to_dict() for e in res.events] == rec[arm]["events"]
     assert rec["speculative"]["final_text"] == rec["baseline"]["final_text"]  # lossless
@@ -82,9 +82,9 @@ def test_judge_tokens_and_reflection_on_the_oracle():
     judge text maps to one id per split word (so a pass costs `judge_cost`),
     known surfaces keep their ids, unknown words hash into the word ids, and the
     verdict is yes > no on the last row of the judge pass."""
-    from paper_2506_15556_b200.model_api import format_judge_prompt
-    from paper_2506_15556_b200.verifier import verify_reflection
-    from paper_2506_15556_b200.vocab import split_words
+    format_judge_prompt = specstream.lm.format_judge_prompt
+    verify_reflection = specstream.verify_reflection
+    split_words = specstream.text.split_words
 
     vocab = SyntheticVocabulary(TINY.vocab)
     ids = vocab.judge_ids("Partial Prompt: w12 w13 . yes")

@@ -9,10 +9,9 @@ import socket
 import torch.multiprocessing as mp
 
 from oracle.decoder import CpuDecoderLM
-from paper_2506_15556_b200.model_api import LatencyModel
+from paper_2506_15556_b200 import LatencyModel, SyntheticVocabulary
 from paper_2506_15556_b200.shapes import TINY
-from paper_2506_15556_b200.simulate import run_sharded
-from paper_2506_15556_b200.vocab import SyntheticVocabulary
+from paper_2506_15556_b200.simulate import ConversationQueue, run_sharded
 from paper_2506_15556_b200.workload import WorkloadSpec, c5_config, synthetic_conversations
 
 SPEC = WorkloadSpec(conversations=5, mean_words=8.0, max_words=14, system_words=4, seed=11)
@@ -53,3 +52,41 @@ def test_sharded_outputs_identical_for_any_world_size(tmp_path):
     assert a.keys() == b.keys() and len(a) == len(rows) + 2
     for k in a:
         assert a[k] == b[k], k
+
+
+def _queue_worker(rank, world, port, out_dir):
+    import json
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q = ConversationQueue(37, world)
+    got = []
+    while (i := q.claim()) is not None:
+        got.append(i)
+    # a second queue on the same store starts from zero again
+    q2 = ConversationQueue(3, world)
+    got2 = []
+    while (i := q2.claim()) is not None:
+        got2.append(i)
+    dist.barrier()
+    with open(f"{out_dir}/r{rank}.json", "w") as fh:
+        json.dump([got, got2], fh)
+    dist.destroy_process_group()
+
+
+def test_dynamic_queue_claims_each_conversation_once(tmp_path):
+    import json
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_queue_worker, args=(3, port, str(tmp_path)), nprocs=3, join=True)
+    parts = [json.loads((tmp_path / f"r{r}.json").read_text()) for r in range(3)]
+    first = sorted(i for p in parts for i in p[0])
+    second = sorted(i for p in parts for i in p[1])
+    assert first == list(range(37)) and second == list(range(3))
+    for p in parts:  # claims are increasing per rank
+        assert p[0] == sorted(p[0])
+    local = ConversationQueue(2)
+    assert [local.claim(), local.claim(), local.claim()] == [0, 1, None]

@@ -21,12 +21,12 @@ ctx = [int(t) for t in rng.integers(4, LLAMA3_8B.vocab, ctxlen)]
 lm.decode_greedy_fused(ctx, 8)
 ms = []
 for i in range(4):
-    lm.discard_after(ctxlen)
+    lm.truncate(ctxlen)
     ms += [c for _, c in lm.decode_greedy_fused(ctx, 40)[1:]]
 cand = [int(t) for t in rng.integers(4, LLAMA3_8B.vocab, 64)]
 v = []
 for i in range(7):
-    lm.discard_after(ctxlen - 8)
+    lm.truncate(ctxlen - 8)
     v.append(lm.verify_greedy_detail(ctx, cand)["gpu_ms"])
 print("RESULT", pkg.__file__, round(statistics.median(ms), 4), round(statistics.median(v), 4))
 '''

@@ -20,12 +20,12 @@ ctx = [int(t) for t in rng.integers(4, shape.vocab, 128)]
 lm.decode_greedy_fused(ctx, 4)
 dec = []
 for _ in range(3):
-    lm.discard_after(128)
+    lm.truncate(128)
     dec += [c for _, c in lm.decode_greedy_fused(ctx, 24)[1:]]
 cand = [int(t) for t in rng.integers(4, shape.vocab, 64)]
 ver = []
 for _ in range(5):
-    lm.discard_after(120)
+    lm.truncate(120)
     ver.append(lm.verify_greedy_detail(ctx, cand)["gpu_ms"])
 floor = shape.weight_bytes_per_pass() / 6531.9e9 * 1e3
 d, v = statistics.median(dec), statistics.median(ver)

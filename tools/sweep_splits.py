@@ -16,12 +16,12 @@ ctx = [int(t) for t in rng.integers(4, LLAMA3_8B.vocab, 128)]
 lm.decode_greedy_fused(ctx, 8)
 ms = []
 for i in range(3):
-    lm.discard_after(128)
+    lm.truncate(128)
     ms += [c for _, c in lm.decode_greedy_fused(ctx, 40)[1:]]
 cand = [int(t) for t in rng.integers(4, LLAMA3_8B.vocab, 64)]
 v = []
 for i in range(5):
-    lm.discard_after(120)
+    lm.truncate(120)
     v.append(lm.verify_greedy_detail(ctx, cand)["gpu_ms"])
 print("RESULT", statistics.median(ms), statistics.median(v))
 ''' % ROOT

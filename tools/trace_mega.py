@@ -12,7 +12,7 @@ rng = np.random.default_rng(0)
 toks = [int(t) for t in rng.integers(4, shape.vocab, int(sys.argv[1]) if len(sys.argv) > 1 else 100)]
 lm.forward(toks)
 for rep in range(3):
-    lm.discard_after(len(toks))
+    lm.truncate(len(toks))
     steps = lm.decode_greedy_fused(toks, 3)
 NS = 16
 names = ["EMB"] + [k for l in range(shape.layers) for k in ("QKV", "ATT", "O", "GU", "D")] + ["LM", "FIN"]
@@ -44,12 +44,12 @@ def report(tr, label):
 
 print("decode step ms", [round(c, 3) for _, c in steps])
 report(grab(), "decode")
-lm.discard_after(len(toks) - 8)
+lm.truncate(len(toks) - 8)
 v = lm.verify_greedy_detail(toks, [5] * 64)
 print("verify gpu ms", v["gpu_ms"])
 report(grab(), "verify")
 # per-CTA straggler view of the decode step (slot 4 = last accumulator seen)
-lm.discard_after(len(toks))
+lm.truncate(len(toks))
 lm.decode_greedy_fused(toks, 2)
 tr = grab()
 for p in (6, 8, 9, 10):  # layer-1 QKV, O, GU, D
