@@ -25,6 +25,10 @@ Two phases, because the two BASELINE metrics need two clocks:
    over a fixed set of conversations: p50 verify-step latency, decode-step
    latency, p50/p90 simulated TTFS, each with its HBM-roofline fraction.
 
+`bf16_agreement` (rank 0): argmax agreement of one 72-row verify pass with
+the layer-streamed float64 oracle (oracle/parity.py) — the oracle as the
+checker of what was timed, not part of any timed region.
+
 `--impl reference` (and `cpu_baseline`): the reference has no decoder (its LM
 is a hash table, lm.py:216-243), so its CPU path for this workload is the
 oracle decoder (oracle/decoder.py, numpy fp32, all host threads) pricing the
@@ -64,6 +68,7 @@ def parse(argv=None):
     ap.add_argument("--shape", default="llama-3-8b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-agreement", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     return ap.parse_args(argv)
 
@@ -424,6 +429,17 @@ def main(argv=None):
                            "conversations": [TTFS_CONVERSATIONS.start, TTFS_CONVERSATIONS.stop - 1],
                            "cost": "measured (CUDA-event ms of every pass)"}
         lm.cost_mode = "modeled"
+
+    # -- bf16 argmax agreement at this shape (rank 0): the oracle as the checker ----------------
+    if rank == 0 and not args.no_agreement and shape.mode == 1:
+        from oracle.parity import fullshape_agreement
+        rec = fullshape_agreement(lm, shape, seed=0, tau=0.1)
+        line["bf16_agreement"] = {k: rec[k] for k in (
+            "rate", "rows_gap_gt_tau", "tau", "rows", "rate_all_rows", "max_abs_logit_diff", "mean_abs_logit_diff",
+            "mismatch_gaps", "shape", "ctx", "window")}
+        line["bf16_agreement"]["how"] = ("one 72-row verify pass over a 128-token prompt vs the layer-streamed "
+                                         "float64 oracle with the GPU's bf16 rounding points (oracle/parity.py); "
+                                         "rate over rows whose oracle top-2 gap > tau, lowest-id ties")
 
     # -- roofline of the dominant kernel: the decode megakernel pass --------------------------
     prof = lm.profile_decode(steps=8)

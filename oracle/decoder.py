@@ -40,11 +40,37 @@ MODE_F32 = 0
 MODE_BF16 = 1
 
 
+class GeneratorWeights:
+    """Weights from the counter-based generator (oracle/weights.py): bit-identical to
+    what csrc/init.cu writes into HBM."""
+
+    def __init__(self, seed: int, bf16: bool):
+        self.seed, self.bf16 = seed, bf16
+
+    def tensor(self, tid: int, shape) -> np.ndarray:
+        return W.tensor(self.seed, tid, shape, self.bf16)
+
+    def rows(self, tid: int, lo: int, hi: int, cols: int) -> np.ndarray:
+        w = W.uniform_f32(self.seed, tid, (hi - lo) * cols, first=lo * cols)
+        if self.bf16:
+            w = W.bf16_bits_to_f32(W.f32_to_bf16_bits(w))
+        return w.astype(np.float64).reshape(hi - lo, cols)
+
+
 class DecoderOracle:
-    """Weights + an incremental KV cache for one token sequence."""
+    """Weights + an incremental KV cache for one token sequence.
+
+    `weights` supplies the stored values (default: the generator). With
+    `stream=True` nothing is kept resident: every layer's matrices are fetched
+    when the layer runs and dropped after it, the embedding is gathered per
+    token and the LM head is applied in row blocks, so a full 8B-shape pass
+    needs about one layer of float64 weights in host memory (SURVEY §8c,
+    the layer-streamed oracle of tests/test_gpu_fullshape.py)."""
+
+    HEAD_BLOCK = 8192
 
     def __init__(self, shape: dict, seed: int = 0, dtype=np.float64, max_layers: int | None = None,
-                 share_layer_weights: bool = False):
+                 share_layer_weights: bool = False, weights=None, stream: bool = False):
         self.s = dict(shape)
         self.seed = seed
         self.dtype = dtype
@@ -56,39 +82,26 @@ class DecoderOracle:
         self.I = s["intermediate"]
         self.L = s["layers"]
         self.eps = s["rms_eps"]
-
-        def t(tid, shp):
-            return W.tensor(seed, tid, shp, self.bf16).astype(dtype)
-
-        self.embed = t(W.TID_EMBED, (V, H))
-        self.head = self.embed if s["tied_embeddings"] else t(W.TID_LM_HEAD, (V, H))
-        qd, kvd = self.nh * self.hd, self.nkv * self.hd
-        self.layers = []
-        n_build = self.L if max_layers is None else min(self.L, max_layers)
-        for l in range(n_build):
-            if share_layer_weights and l > 0:
-                self.layers.append(self.layers[0])
-                continue
-            lay = {
-                "wq": t(W.layer_tid(l, W.WQ), (qd, H)),
-                "wk": t(W.layer_tid(l, W.WK), (kvd, H)),
-                "wv": t(W.layer_tid(l, W.WV), (kvd, H)),
-                "wo": t(W.layer_tid(l, W.WO), (H, qd)),
-                "wg": t(W.layer_tid(l, W.WGATE), (self.I, H)),
-                "wu": t(W.layer_tid(l, W.WUP), (self.I, H)),
-                "wd": t(W.layer_tid(l, W.WDOWN), (H, self.I)),
-            }
-            if s["qkv_bias"]:
-                lay["bq"] = t(W.layer_tid(l, W.BQ), (qd,))
-                lay["bk"] = t(W.layer_tid(l, W.BK), (kvd,))
-                lay["bv"] = t(W.layer_tid(l, W.BV), (kvd,))
-            self.layers.append(lay)
-        if share_layer_weights:
-            # timing-only mode (bench cpu_baseline): every layer streams layer 0's
-            # weights, so per-pass memory traffic matches the full model.
-            while len(self.layers) < self.L:
-                self.layers.append(self.layers[0])
-        self.n_layers_run = len(self.layers)
+        self.src = weights if weights is not None else GeneratorWeights(seed, self.bf16)
+        self.stream = stream
+        self.n_layers_run = self.L if max_layers is None else min(self.L, max_layers)
+        self.share = share_layer_weights
+        self._head_tid = W.TID_EMBED if s["tied_embeddings"] else W.TID_LM_HEAD
+        if not stream:
+            self.embed = self.src.tensor(W.TID_EMBED, (V, H)).astype(dtype)
+            self.head = self.embed if s["tied_embeddings"] else self.src.tensor(W.TID_LM_HEAD, (V, H)).astype(dtype)
+            self.layers = []
+            for l in range(self.n_layers_run):
+                if share_layer_weights and l > 0:
+                    self.layers.append(self.layers[0])
+                    continue
+                self.layers.append(self._load_layer(l))
+            if share_layer_weights:
+                # timing-only mode (bench cpu_baseline): every layer streams layer 0's
+                # weights, so per-pass memory traffic matches the full model.
+                while len(self.layers) < self.L:
+                    self.layers.append(self.layers[0])
+            self.n_layers_run = len(self.layers)
 
         self.bias = np.zeros(V, dtype=dtype)
         sigma = 0.02 * np.sqrt(H)
@@ -99,11 +112,42 @@ class DecoderOracle:
         self.inv_freq = s["rope_theta"] ** (-(np.arange(half, dtype=np.float64) * 2.0) / self.hd)
         self.reset()
 
+    def _load_layer(self, l: int) -> dict:
+        H, qd, kvd = self.H, self.nh * self.hd, self.nkv * self.hd
+
+        def t(which, shp):
+            return self.src.tensor(W.layer_tid(l, which), shp).astype(self.dtype)
+
+        lay = {"wq": t(W.WQ, (qd, H)), "wk": t(W.WK, (kvd, H)), "wv": t(W.WV, (kvd, H)), "wo": t(W.WO, (H, qd)),
+               "wg": t(W.WGATE, (self.I, H)), "wu": t(W.WUP, (self.I, H)), "wd": t(W.WDOWN, (H, self.I))}
+        if self.s["qkv_bias"]:
+            lay["bq"] = t(W.BQ, (qd,))
+            lay["bk"] = t(W.BK, (kvd,))
+            lay["bv"] = t(W.BV, (kvd,))
+        return lay
+
+    def _layer(self, l: int) -> dict:
+        return self._load_layer(l) if self.stream else self.layers[l]
+
+    def _embed(self, tokens) -> np.ndarray:
+        if not self.stream:
+            return self.embed[np.asarray(tokens, dtype=np.int64)].astype(self.dtype)
+        return np.stack([self.src.rows(W.TID_EMBED, int(t), int(t) + 1, self.H)[0] for t in tokens]).astype(self.dtype)
+
+    def _head(self, hn) -> np.ndarray:
+        if not self.stream:
+            return hn @ self.head.T
+        out = np.empty((hn.shape[0], self.V), dtype=self.dtype)
+        for lo in range(0, self.V, self.HEAD_BLOCK):
+            hi = min(self.V, lo + self.HEAD_BLOCK)
+            out[:, lo:hi] = hn @ self.src.rows(self._head_tid, lo, hi, self.H).astype(self.dtype).T
+        return out
+
     # -- state -----------------------------------------------------------------
     def reset(self) -> None:
         self.tokens: list[int] = []
-        self.k = [np.zeros((self.nkv, 0, self.hd), dtype=self.dtype) for _ in self.layers]
-        self.v = [np.zeros((self.nkv, 0, self.hd), dtype=self.dtype) for _ in self.layers]
+        self.k = [np.zeros((self.nkv, 0, self.hd), dtype=self.dtype) for _ in range(self.n_layers_run)]
+        self.v = [np.zeros((self.nkv, 0, self.hd), dtype=self.dtype) for _ in range(self.n_layers_run)]
 
     def truncate(self, n: int) -> None:
         self.tokens = self.tokens[:n]
@@ -140,10 +184,11 @@ class DecoderOracle:
         n0 = len(self.tokens)
         Wn = len(new_tokens)
         pos = np.arange(n0, n0 + Wn)
-        x = self.embed[np.asarray(new_tokens, dtype=np.int64)].astype(self.dtype)
+        x = self._embed(new_tokens)
         scale = 1.0 / np.sqrt(self.hd)
         grp = self.nh // self.nkv
-        for li, lay in enumerate(self.layers):
+        for li in range(self.n_layers_run):
+            lay = self._layer(li)
             xn, sc_in = self._operand(x)
             q = (xn @ lay["wq"].T) * sc_in
             k = (xn @ lay["wk"].T) * sc_in
@@ -177,7 +222,7 @@ class DecoderOracle:
             x = x + a @ lay["wd"].T
         self.tokens.extend(int(t) for t in new_tokens)
         hn, sc_in = self._operand(x)
-        logits = (hn @ self.head.T) * sc_in + self.bias
+        logits = self._head(hn) * sc_in + self.bias
         return hn, logits
 
     def ensure(self, context: list[int]) -> None:

@@ -56,15 +56,15 @@ def scale_f32(std: float) -> np.float32:
 
 
 def uniform_f32(seed: int, tid: int, count: int, std: float = 0.02,
-                chunk: int = 1 << 24) -> np.ndarray:
-    """`count` fp32 weights of tensor `tid`, identical to init.cu's output."""
+                chunk: int = 1 << 24, first: int = 0) -> np.ndarray:
+    """`count` fp32 weights of tensor `tid` from element `first` on, identical to init.cu's output."""
     key = _key(seed, tid)
     scale = scale_f32(std)
     out = np.empty(count, dtype=np.float32)
     with np.errstate(over="ignore"):
         for lo in range(0, count, chunk):
             hi = min(count, lo + chunk)
-            idx = np.arange(lo + 1, hi + 1, dtype=np.uint64)
+            idx = np.arange(first + lo + 1, first + hi + 1, dtype=np.uint64)
             h = _mix(key + idx * G)
             u = (h >> np.uint64(41)).astype(np.int64) - (1 << 22)
             out[lo:hi] = u.astype(np.float32) * scale

@@ -102,3 +102,26 @@ def test_judge_tokens_and_reflection_on_the_oracle():
     assert out.judge_fallback in (None, "judge_rejected")
     if out.judge_fallback is None:
         assert out.accepted_count == 3 and out.first_sentence_accepted
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("tied", [False, True])
+def test_streamed_oracle_equals_resident(mode, tied):
+    """The layer-streamed oracle (weights fetched per layer, embedding gathered per
+    token, LM head in row blocks) computes exactly what the resident one does."""
+    shape = small_shape(mode=mode, vocab=700, tied_embeddings=tied).as_dict()
+    toks = [int(t) for t in np.random.default_rng(1).integers(4, 700, 24)]
+    a = DecoderOracle(shape, seed=5)
+    b = DecoderOracle(shape, seed=5, stream=True)
+    b.HEAD_BLOCK = 256  # several head blocks, one partial
+    _, la = a.extend(toks[:10])
+    _, lb = b.extend(toks[:10])
+    np.testing.assert_array_equal(la, lb)
+    _, la = a.extend(toks[10:])
+    _, lb = b.extend(toks[10:])
+    np.testing.assert_array_equal(la, lb)
+
+
+def test_generator_offset_rows():
+    full = W.uniform_f32(3, 9, 5000)
+    np.testing.assert_array_equal(W.uniform_f32(3, 9, 1200, first=1700), full[1700:2900])
