@@ -1169,7 +1169,7 @@ __device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, in
 template <class ES>
 __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, int layer, int n0, int w, int lane,
                                                  const DefTile& T, float* S, int cap_floats, uint32_t wbar,
-                                                 uint32_t& wphase, ES& es) {
+                                                 uint32_t& wphase, ES& es, int trace_p = -1) {
   const int tid = threadIdx.x - 64;
   const int np = T.npieces;
   const bool has_x = kind == PH_O || kind == PH_D;
@@ -1184,6 +1184,7 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
     float* X = S + np * nb * 128;
     if (tid == 0) {
       fence_proxy_async_global();  // generic writes of other CTAs (acquired) -> async-proxy reads
+      if (trace_p >= 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
       const uint32_t bytes = uint32_t(np * nb * 512 + (has_x ? nb * 512 : has_rope ? nb * rope_row * 4 : 0));
       mbar_expect_tx(wbar, bytes);
       for (int pc = 0; pc < np; ++pc)
@@ -1193,9 +1194,11 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
         for (int r = 0; r < nb; ++r) bulk_g2s(smem_u32(X + r * 128), P.x + size_t(b0 + r) * P.H + T.tile * 128, 512, wbar);
       else if (has_rope)
         bulk_g2s(smem_u32(X), P.rope + size_t(n0 + b0) * half, uint32_t(nb * rope_row * 4), wbar);
+      if (trace_p >= 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 3);
     }
     mbar_wait(wbar, wphase);
     wphase ^= 1u;
+    if (trace_p >= 0 && tid == 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 14);
     for (int r = w; r < nb; r += kWorkerWarps) {
       const int t = b0 + r;
       float4 acc = *reinterpret_cast<const float4*>(S + r * 128 + f0);
@@ -1208,6 +1211,7 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
       }
       vec_finish_row(P, kind, layer, n0, w, lane, T.tile, t, acc, X + r * (has_x ? 128 : rope_row), es);
     }
+    if (trace_p >= 0 && tid == 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 15);
     wk_bar();  // the staging area is reused by the next batch / tile
   }
 }
@@ -1681,7 +1685,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
 #pragma unroll
           for (int d = 0; d < 2; ++d)
             if (d < nd && D[d].r_lo < D[d].r_hi)
-              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, wbar, wphase, es);
+              finish_share_vec(P, kind, layer, n0, w, lane, D[d], stage, cap, wbar, wphase, es, d == 0 ? p : -1);
           if (tid == 0) stamp(P, p, c, G, 9);
           finalized = true;
         };
@@ -1808,7 +1812,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
             const int tile = i0 / rows, r0 = i0 - tile * rows, r1 = min(rows, e - tile * rows);
             const int c_first = sk_owner(tile * g.KB, g.G, g.T), c_last = sk_owner((tile + 1) * g.KB - 1, g.G, g.T);
             const DefTile T{tile, c_first, c_last - c_first + 1, r0, r1, first_piece_slot(c_first, tile, g)};
-            finish_share_vec(P, kind, layer, n0, w, lane, T, stage, cap, wbar, wphase, es);
+            finish_share_vec(P, kind, layer, n0, w, lane, T, stage, cap, wbar, wphase, es, i0 == a ? p : -1);
             i0 = tile * rows + r1;
           }
           if (tid == 0) stamp(P, p, c, G, 9);

@@ -34,7 +34,7 @@ def report(tr, label):
         start = np.nanmax(tr[p - 1, :, 2])
         a = agg[names[p]]
         a["span"].append(np.nanmax(tr[p, :, 2]) - start)
-        for slot, key in ((0, "prod_bar"), (12, "prod_done"), (13, "mma_done"), (1, "bar"), (3, "offs"), (4, "acc_last"), (5, "published"), (7, "waited|a_start"), (8, "a_loaded"), (14, "a_S"), (15, "a_softmax"), (9, "a_computed"), (10, "a_counted"), (11, "a_merged"), (6, "deferred")):
+        for slot, key in ((0, "prod_bar"), (12, "prod_done"), (13, "mma_done"), (1, "bar"), (3, "fin_issued"), (4, "acc_last"), (5, "published"), (7, "waited|a_start"), (8, "a_loaded"), (14, "a_S|fin_landed"), (15, "a_softmax|fin_computed"), (9, "a_computed"), (10, "a_counted|fin_fenced"), (11, "a_merged"), (6, "deferred")):
             col = tr[p, :, slot]
             if np.isfinite(col).any():
                 a[key + "_max"].append(np.nanmax(col) - start)
