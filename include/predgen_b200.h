@@ -112,7 +112,8 @@ int ps_verify_topk(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const 
 /* Greedy continuation of seq[0..n_seq): up to max_tokens argmax tokens, the
  * first from row n_seq-1 (free when already resident), the rest from
  * back-to-back 1-row decode steps replayed from a CUDA graph without host
- * round trips; stops after EOS when stop_at_eos. token_ms (nullable) gets the
+ * round trips; stops after EOS when stop_at_eos, and at the KV capacity
+ * (max_seq positions: *n_out < max_tokens without an error). token_ms (nullable) gets the
  * measured device ms attributable to each produced token. The last produced
  * token is not resident. Replaces the decode loop of `ar_generate`
  * (generate.py:163-176) / `greedy_decode` (lm.py:373-381). */

@@ -35,8 +35,10 @@ def nvcc() -> str:
 
 
 def _flags() -> list[str]:
+    # PS_DEBUG=1: bounded spin waits that trap instead of hanging (tc_common.cuh)
+    debug = ["-DPS_DEBUG_SPIN"] if os.environ.get("PS_DEBUG") == "1" else []
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                   f"-I{INCLUDE}", f"-I{CSRC}"]
+                   f"-I{INCLUDE}", f"-I{CSRC}"] + debug
 
 
 def _digest() -> str:

@@ -149,7 +149,8 @@ struct MegaParams {
   float* o_part;
   float* ml_part;
   unsigned* acnt;
-  float* part;              // [G][2][kMaxWindow][128] stream-K piece partials (u64 tagged for <= 8 rows)
+  float* part;              // [G][2][kMaxWindow][128] stream-K piece partials (wide passes)
+  unsigned long long* tags; // [G][2][128] (tag, fp32) piece partials of 1-row passes
   unsigned* epoch;          // pass counter (partial tags), advanced by CTA 0 at the end of each pass
   unsigned* tile_cnt;       // [phase][max_tiles], zeroed before the pass
   int max_tiles;

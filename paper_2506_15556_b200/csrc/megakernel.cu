@@ -101,7 +101,9 @@ __device__ __forceinline__ void grid_arrive(unsigned* bar) {
 // Acquire-load polling. (Relaxed polling plus one fence after the target is
 // seen measured slower: +1.2% decode, +3% verify — DESIGN.md.)
 __device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
+  PS_SPIN_START;
   while (ld_acquire_gpu(bar) < target) {
+    PS_SPIN_CHECK;  // debug builds: bounded (tc_common.cuh)
   }
 }
 
@@ -1007,6 +1009,7 @@ __device__ __forceinline__ void attn_count_merge(const MegaParams& P, int n0, in
 // tile, every CTA after c_first starts its range inside the tile (slot 0);
 // c_first's piece is its first tile only when its range starts on the tile.
 __device__ __forceinline__ int piece_off_slot(int cc, int slot, int m) { return (cc * 2 + slot) * kMaxWindow * 128 + m; }
+__device__ __forceinline__ int tag_off_slot(int cc, int slot, int m) { return (cc * 2 + slot) * 128 + m; }
 __device__ __forceinline__ int first_piece_slot(int c_first, int tile, const Gemm& g) {
   return sk_start(c_first, g.G, g.T) == tile * g.KB ? 0 : 1;
 }
@@ -1035,20 +1038,22 @@ template <class ES>
 __device__ __forceinline__ void finish_tagged(const MegaParams& P, int kind, int layer, int n0, int tile, int m, int q,
                                               int lane, int c_first, int npieces, const Gemm& g, unsigned tag, float own,
                                               ES& es) {
-  const unsigned long long* part = reinterpret_cast<const unsigned long long*>(P.part);
+  const unsigned long long* part = P.tags;
   EpiPre pre;
   epi_load<1>(P, kind, 1, n0, tile, m, 0, pre);
   unsigned long long w[7];
 #pragma unroll
   for (int pc = 1; pc < 8; ++pc)
-    if (pc < npieces) w[pc - 1] = ld_tagged(part + piece_off_slot(c_first + pc, 0, m));
+    if (pc < npieces) w[pc - 1] = ld_tagged(part + tag_off_slot(c_first + pc, 0, m));
   bool again = true;
+  PS_SPIN_START;
   while (again) {
+    PS_SPIN_CHECK;
     again = false;
 #pragma unroll
     for (int pc = 1; pc < 8; ++pc)
       if (pc < npieces && unsigned(w[pc - 1] >> 32) != tag) {
-        w[pc - 1] = ld_tagged(part + piece_off_slot(c_first + pc, 0, m));
+        w[pc - 1] = ld_tagged(part + tag_off_slot(c_first + pc, 0, m));
         again = true;
       }
   }
@@ -1754,7 +1759,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
             if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
             finish_tagged(P, kind, layer, n0, tile, m, q, lane, c_first, npieces, g, tag0 + unsigned(p), v[0], es);
           } else if (!spread) {
-            unsigned long long* mine = reinterpret_cast<unsigned long long*>(P.part) + piece_off_slot(c, pj == 0 ? 0 : 1, m);
+            unsigned long long* mine = P.tags + tag_off_slot(c, pj == 0 ? 0 : 1, m);
             float v[8];
             tmem_ld8(trow, v);
             st_tagged(mine, tag0 + unsigned(p), v[0]);

@@ -192,7 +192,11 @@ struct ps_handle {
   int* d_res = nullptr;
   PassCtx* d_ctx = nullptr;
   PassCtx* d_ctx_aux = nullptr;
-  float* logits_buf = nullptr;
+  float* logits_buf = nullptr;  // [kMaxWindow][v_count] fp32 logits (parity rows, top-k ranks)
+  // top-k verify: the pass itself writes its rows' logits into logits_buf (no
+  // LM-head re-run); cap_n0 / cap_rows = the positions the last chunk covered
+  bool capture_logits = false;
+  int cap_n0 = -1, cap_rows = 0;
   // bf16 chain state
   float* rstd = nullptr;        // [kMaxWindow] rstd of the current residual rows
   float* rstd_cache = nullptr;  // [seq_rows] rstd of the final hidden per position
@@ -207,6 +211,7 @@ struct ps_handle {
   std::vector<int> xmaps_ready;             // per ntok/16
   __nv_bfloat16* qkv_bias_all = nullptr;
   float* mega_part = nullptr;
+  unsigned long long* mega_tags = nullptr;  // [sms][2][128] tagged decode partials
   unsigned* mega_cnt = nullptr;             // [0]=bar, [1]=lm_cnt, [2]=bar2, [64..] per-phase tile counters
   int mega_max_tiles = 0;
   size_t mega_cnt_words = 0;
@@ -339,6 +344,11 @@ void prof_mark(ps_handle* h, int cls) {
 
 void enqueue_shard_merge(ps_handle* h, PassCtx* ctx, int max_rows, bool decode);
 
+// Passes produce packed (max, lowest id) keys and join them across shards when
+// the LM head is vocab-sharded, or when a communicator is attached to a
+// one-shard instance (a 1-rank NCCL world: the whole join path on one GPU).
+bool keyed(const ps_handle* h) { return h->cfg.vocab_shards > 1 || h->nccl_comm != nullptr; }
+
 // One forward pass of the decoder body + LM head + argmax over `max_rows`
 // rows at ctx->n0 (device-side). tok_in == nullptr selects decode mode.
 template <typename T>
@@ -387,8 +397,9 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
   }
   prof_mark(h, 6);
   launch_lmhead_f32(ctx, max_rows, static_cast<const float*>(h->hn_cache), 0, static_cast<const float*>(h->head),
-                      h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val, h->am_idx, nullptr, 0, st);
-  const bool sharded = h->cfg.vocab_shards > 1;
+                      h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val, h->am_idx,
+                      h->capture_logits ? h->logits_buf : nullptr, h->capture_logits ? h->v_count : 0, st);
+  const bool sharded = keyed(h);
   launch_argmax_reduce(ctx, max_rows, h->am_val, h->am_idx, h->am_tiles, h->argmax_pos, sharded ? h->keys : nullptr,
                        st);
   if (sharded) enqueue_shard_merge(h, ctx, max_rows, false);
@@ -396,7 +407,7 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
 }
 
 int launches_per_pass(const ps_handle* h) {
-  if (h->mega) return 1 + (h->cfg.vocab_shards > 1 ? 1 : 0);
+  if (h->mega) return 1 + (keyed(h) ? 1 : 0);
   return 1 + 10 * h->L + 2;
 }
 
@@ -423,7 +434,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   MegaParams P{};
   P.ctx = ctx;
   P.decode = decode ? 1 : 0;
-  const bool sharded = h->cfg.vocab_shards > 1;
+  const bool sharded = keyed(h);
   P.advance = (decode && !sharded) ? 1 : 0;
   P.tok_in = tok_in;
   P.L = h->L; P.H = h->H; P.qd = h->qd; P.kvd = h->kvd; P.I = h->I; P.hd = h->hd;
@@ -474,6 +485,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.ml_part = h->ml_part;
   P.acnt = h->acnt;
   P.part = h->mega_part;
+  P.tags = h->mega_tags;
   P.epoch = h->mega_epoch;
   P.tile_cnt = h->mega_cnt + 64;
   P.max_tiles = h->mega_max_tiles;
@@ -484,7 +496,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.bar = h->mega_cnt;
   P.bar2 = h->mega_cnt + 2;
   P.lm_only = lm_only ? 1 : 0;
-  P.logits_out = logits_out;
+  P.logits_out = (logits_out == nullptr && h->capture_logits && !lm_only) ? h->logits_buf : logits_out;
   P.ld_logits = h->v_count;
   P.trace = h->mega_trace;
   {
@@ -570,6 +582,10 @@ int enqueue_extend(ps_handle* h, const int* tokens, int n, int* base_out) {
     CK(copy_async(h, h->d_tok, ht, sizeof(int) * rows, cudaMemcpyHostToDevice));
     enqueue_pass_any(h, h->d_ctx, rows, h->d_tok, base + done + rows - 1);
     CK(cudaGetLastError());
+    if (h->capture_logits) {
+      h->cap_n0 = base + done;
+      h->cap_rows = rows;
+    }
     h->stats.passes += 1;
     h->stats.rows += rows;
     done += rows;
@@ -686,6 +702,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     return fail(PS_ERR_INVALID, "unsupported decoder shape");
   const int shards = std::max(1, c.vocab_shards);
   if (c.shard_rank < 0 || c.shard_rank >= shards) return fail(PS_ERR_INVALID, "bad shard rank");
+  // one extend call cycles through the pinned PassCtx/token ring without waiting
+  // (kMaxWindow rows per slot, two slots kept for the verify compare and the read-back)
+  if (c.max_seq > (kCtxSlots - 2) * kMaxWindow)
+    return fail(PS_ERR_INVALID, "max_seq exceeds what one extend call can stage (62 x 256 tokens)");
   CK(cudaSetDevice(c.device));
   ps_handle* h = new ps_handle();
   h->cfg = c;
@@ -732,7 +752,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     std::vector<float> b(V, 0.f);
     b[0] = c.eos_bias;
     for (int i = 1; i < 4; ++i) b[i] = c.term_bias;
-    copy_sync(h, h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
+    if (copy_sync(h, h->lm_bias, b.data(), sizeof(float) * V, cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
   }
   h->layers.resize(h->L);
   if (h->bf16 && c.qkv_bias) {
@@ -888,7 +908,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     int dev_sms = 0;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
     h->sms = dev_sms > 0 ? dev_sms : 148;
-    h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128 * 2);  // room for u64 tagged partials
+    h->mega_part = h->dalloc<float>(size_t(h->sms) * 2 * kMaxWindow * 128);
+    // 1-row passes publish (tag, value) words in a buffer of their own, so a
+    // wide pass's fp32 partials can never be read as a tagged word
+    h->mega_tags = h->dalloc<unsigned long long>(size_t(h->sms) * 2 * 128);
     h->mega_epoch = h->dalloc<unsigned>(1);
     // per-phase counter block: one counter per tile plus the all-split
     // phases' grid-sync counter at index `tiles` (megakernel.cu)
@@ -897,7 +920,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
     h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
-    if (!h->mega_part || !h->mega_epoch || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
+    if (!h->mega_part || !h->mega_tags || !h->mega_epoch || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
     if (const char* tr = std::getenv("PS_TRACE"); tr && tr[0] == '1')
       h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 16);
     std::vector<CUtensorMap> wm(size_t(4) * h->L + 1);
@@ -908,7 +931,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       std::memcpy(&wm[4 * l + 3], h->layers[l].d.tm.bytes, sizeof(CUtensorMap));
     }
     std::memcpy(&wm[4 * h->L], h->tm_head.bytes, sizeof(CUtensorMap));
-    copy_sync(h, h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice);
+    if (copy_sync(h, h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
     std::vector<CUtensorMap> xm(size_t(kMaxWindow / 16) * 4);
     for (int k = 0; k < kMaxWindow / 16; ++k) {
       const ActDescs* ad = act_descs(h, 16 * (k + 1));
@@ -918,7 +941,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
       std::memcpy(&xm[4 * k + 2], ad->act.bytes, sizeof(CUtensorMap));
       std::memcpy(&xm[4 * k + 3], ad->hn.bytes, sizeof(CUtensorMap));
     }
-    copy_sync(h, h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice);
+    if (copy_sync(h, h->d_xmaps, xm.data(), sizeof(CUtensorMap) * xm.size(), cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
     // every pass width must fit one CTA per SM (co-residency of the grid)
     const int grp = h->nh / h->nkv;
     for (int ntok = 16; ntok <= kMaxWindow; ntok += 16)
@@ -939,10 +962,10 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
         const double a = double(p) * inv;
         tab[p * half + i] = make_float2(float(std::cos(a)), float(std::sin(a)));
       }
-    copy_sync(h, h->rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice);
+    if (copy_sync(h, h->rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
     std::vector<unsigned char> tm(V, 0);
     tm[1] = tm[2] = tm[3] = 1;
-    copy_sync(h, h->term_mask, tm.data(), V, cudaMemcpyHostToDevice);
+    if (copy_sync(h, h->term_mask, tm.data(), V, cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
   }
   if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return (ps_destroy(h), fail(PS_ERR_CUDA, "device initialisation failed"));
@@ -1030,13 +1053,20 @@ int verify_impl(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int
   const int n = int(seq.size());
   int computed = 0, base = 0;
   bool enq = false;
+  if (topk > 0 && !h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
   CK(cudaEventRecord(h->ev0, h->st));
-  if (int rc = sync_to(h, seq.data(), n, &computed, &base, &enq, false)) return rc;
+  h->capture_logits = topk > 0;
+  h->cap_n0 = -1;
+  const int sync_rc = sync_to(h, seq.data(), n, &computed, &base, &enq, false);
+  h->capture_logits = false;
+  if (sync_rc) return sync_rc;
   if (n_cand) {
     int slot;
     next_ctx_slot(h, &slot);
     int* ht = h->h_tok + size_t(slot) * kMaxWindow;
-    // candidate may exceed one ring slot: copy through the pinned argmax mirror tail instead
+    // a candidate that fits one ring slot is staged in pinned memory; a longer one
+    // (top-k rejects those, greedy allows up to max_seq) is copied from the
+    // caller's pageable buffer (cudaMemcpyAsync stages it synchronously)
     const int* src = cand;
     if (n_cand <= kMaxWindow) {
       std::memcpy(ht, cand, sizeof(int) * n_cand);
@@ -1046,8 +1076,14 @@ int verify_impl(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int
     launch_verify_compare(h->argmax_pos, n_prompt, h->d_cand, n_cand, h->term_mask, h->d_res, h->st);
     h->stats.launches += 1;
     if (topk > 0) {  // rows n_prompt-1 .. n_prompt+n_cand-2 score the candidate tokens
-      if (int rc = enqueue_logits_rows(h, n_prompt - 1, n_cand)) return rc;
-      launch_topk_rank(h->logits_buf, h->v_count, h->v_count, h->d_cand, n_cand, h->d_res + 4, h->st);
+      const int first = n_prompt - 1;
+      const float* rows = h->logits_buf;
+      if (enq && h->cap_n0 >= 0 && h->cap_n0 <= first && first + n_cand <= h->cap_n0 + h->cap_rows) {
+        rows = h->logits_buf + size_t(first - h->cap_n0) * h->v_count;  // written by this very pass
+      } else {  // rows resident from an earlier pass (or a chunked extend): LM head over them
+        if (int rc = enqueue_logits_rows(h, first, n_cand)) return rc;
+      }
+      launch_topk_rank(rows, h->v_count, h->v_count, h->d_cand, n_cand, h->d_res + 4, h->st);
       h->stats.launches += 1;
     }
     CK(copy_async(h, h->h_res, h->d_res, sizeof(int) * (topk > 0 ? 4 + n_cand : 2), cudaMemcpyDeviceToHost));
@@ -1134,7 +1170,12 @@ int ps_decode_greedy(ps_handle* h, const int32_t* seq, int32_t n_seq, int32_t ma
   std::vector<float> ms(kMaxSteps);
   while (!stopped && produced < max_tokens) {
     const int n0 = int(h->resident.size());
-    const int steps = std::min(kMaxSteps, max_tokens - produced);
+    // never ask for steps past the KV capacity (a request that EOS ends early
+    // must not fail): the loop stops at the capacity with the tokens produced
+    // so far; the next call that needs another position gets PS_ERR_CAPACITY
+    const int room = h->cfg.max_seq - n0;
+    if (room <= 0) break;
+    const int steps = std::min(std::min(kMaxSteps, max_tokens - produced), room);
     int executed = 0;
     if (int rc = run_decode_steps(h, n0, steps, stop_at_eos, &executed, ms.data())) return rc;
     // step i processed token (previous argmax) at position n0+i and produced argmax_pos[n0+i]
@@ -1332,7 +1373,7 @@ int ps_shard_init(ps_handle* h, const void* id, int32_t rank, int32_t world) {
 int ps_shard_keys(ps_handle* h, int32_t first, int32_t n, uint64_t* out) {
   if (!h || !out || first < 0 || n < 0 || first + n > int(h->resident.size()))
     return fail(PS_ERR_INVALID, "rows outside the resident sequence");
-  if (h->cfg.vocab_shards <= 1) return fail(PS_ERR_INVALID, "not a vocab-sharded instance");
+  if (!keyed(h)) return fail(PS_ERR_INVALID, "not a vocab-sharded instance (and no communicator attached)");
   CK(cudaSetDevice(h->cfg.device));
   CK(copy_sync(h, out, h->keys_pos + first, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return PS_OK;

@@ -36,8 +36,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Debug builds (PS_DEBUG_SPIN, `PS_DEBUG=1 python -m paper_2506_15556_b200.build`)
+// bound every spin: a wait that has not completed after ~4 s of SM clocks traps,
+// so a faulting or diverged CTA surfaces as a launch error instead of a hang.
+#ifdef PS_DEBUG_SPIN
+__device__ __forceinline__ void spin_guard(long long t0) {
+  if (clock64() - t0 > (1ll << 33)) __trap();
+}
+#define PS_SPIN_START const long long ps_spin_t0 = clock64()
+#define PS_SPIN_CHECK spin_guard(ps_spin_t0)
+#else
+#define PS_SPIN_START
+#define PS_SPIN_CHECK
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  PS_SPIN_START;
   while (!mbar_try_wait(bar, parity)) {
+    PS_SPIN_CHECK;
   }
 }
 

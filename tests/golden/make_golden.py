@@ -159,40 +159,80 @@ def make_tiny():
     print("tiny verify cases:", len(K), "k:", K)
 
 
-def make_c2(n_turns: int = 1):
-    """Config c2: Qwen2.5-0.5B shape, fp32, 128-token query in 16 chunks, cap 64."""
+def _turn_record(lm, cfg, turns, conv_id):
+    """The reference's run_conversation on `lm` (speculative and baseline arms)."""
+    rec = {}
+    for baseline in (False, True):
+        lm.min_gap = np.inf
+        res = ref.run_conversation(turns, cfg, lm, conversation_id=conv_id, baseline=baseline)
+        rec["baseline" if baseline else "speculative"] = [
+            {"final_text": r.final_text, "nfe_total": r.nfe_total, "events": events_json(r)} for r in res]
+        rec["min_gap_" + ("baseline" if baseline else "speculative")] = float(lm.min_gap)
+    return rec
+
+
+def make_c2(n_conv: int = 4):
+    """Config c2: Qwen2.5-0.5B shape, fp32, 128-token query in 16 chunks, cap 64.
+    Conversations 0 and 2 have a second turn (the reply goes into the history)."""
     from paper_2506_15556_b200.shapes import QWEN_05B
     shape = QWEN_05B.as_dict()
     vocab = SyntheticVocabulary(QWEN_05B.vocab)
     cfg = RefConfig(system_prompt="", chunk_words=8, max_response_tokens=64)
-    turns, trial = [], 0
+    convs, trial = [], 0
     lm = CpuDecoderLM(shape, vocab, seed=0, latency=ref_lm.LatencyModel())
-    while len(turns) < n_turns and trial < 6:
+    while len(convs) < n_conv and trial < 12:
         rng = np.random.default_rng(9000 + trial)
-        text = tiny_prompt(rng, vocab, 128)
-        rec = {"trial": trial, "prompt": text}
-        ok = True
-        for baseline in (False, True):
-            lm.min_gap = np.inf
-            run = ref.run_baseline if baseline else ref.run_turn
-            res = run([], ref.make_stream(text, cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
-            rec["baseline" if baseline else "speculative"] = {
-                "final_text": res.final_text, "nfe_total": res.nfe_total, "events": events_json(res),
-                "min_gap": float(lm.min_gap)}
-            ok = ok and lm.min_gap > GAP_MIN
-            print("c2 trial", trial, "baseline" if baseline else "spec", "passes", lm.passes, "gap", lm.min_gap,
-                  flush=True)
+        turns = [tiny_prompt(rng, vocab, 128)]
+        if len(convs) % 2 == 0:
+            turns.append(tiny_prompt(rng, vocab, 48))
+        rec = {"trial": trial, "turns": turns, **_turn_record(lm, cfg, turns, f"c2-{trial}")}
+        ok = min(rec["min_gap_speculative"], rec["min_gap_baseline"]) > GAP_MIN
+        print("c2 trial", trial, "turns", len(turns), "gap", rec["min_gap_speculative"], rec["min_gap_baseline"],
+              "kept" if ok else "skipped", flush=True)
         if ok:
-            turns.append(rec)
+            convs.append(rec)
         trial += 1
-    (HERE / "c2_turns.json").write_text(json.dumps({"shape": shape, "config": "c2", "seed": 0, "turns": turns},
-                                                   sort_keys=True) + "\n")
-    print("c2 turns kept:", len(turns), "of", trial)
+    (HERE / "c2_turns.json").write_text(json.dumps({"shape": shape, "config": "c2", "seed": 0,
+                                                   "conversations": convs}, sort_keys=True) + "\n")
+    print("c2 conversations kept:", len(convs), "of", trial)
+
+
+def make_tiny_topk(n_turns: int = 5):
+    """Config c1 with the reference's top-k verifier (k = 3, verify.py:100-113):
+    event logs of `run_turn` on the float64 oracle decoder. A top-k decision
+    depends on where the candidate token ranks, not only on the top-2 gap, so a
+    turn is kept only if the float32 oracle (a different accumulation) gives the
+    identical event log — the decisions are not near a rank boundary."""
+    shape = TINY.as_dict()
+    vocab = SyntheticVocabulary(TINY.vocab)
+    cfg = RefConfig(system_prompt="", chunk_words=8, max_response_tokens=32, verifier="topk", topk_k=3)
+    turns, trial = [], 0
+    while len(turns) < n_turns and trial < 40:
+        rng = np.random.default_rng(7700 + trial)
+        text = tiny_prompt(rng, vocab, 64)
+        logs = []
+        for dtype in (np.float64, np.float32):
+            lm = CpuDecoderLM(shape, vocab, seed=0, latency=ref_lm.LatencyModel(), dtype=dtype)
+            res = ref.run_turn([], ref.make_stream(text, cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+            logs.append({"final_text": res.final_text, "nfe_total": res.nfe_total, "events": events_json(res),
+                         "min_gap": float(lm.min_gap)})
+        ks = [e["k"] for e in logs[0]["events"] if e["kind"] == "verify"]
+        ok = logs[0]["events"] == logs[1]["events"] and logs[0]["min_gap"] > GAP_MIN
+        print("topk trial", trial, "k per round", ks, "kept" if ok else "skipped", flush=True)
+        if ok:
+            turns.append({"trial": trial, "prompt": text, "speculative": logs[0]})
+        trial += 1
+    (HERE / "tiny_topk_turns.json").write_text(json.dumps({"shape": shape, "config": "c1-topk3", "seed": 0,
+                                                          "turns": turns}, sort_keys=True) + "\n")
+    print("topk turns kept:", len(turns), "of", trial)
 
 
 if __name__ == "__main__":
     if "--c2" in sys.argv:
         make_c2()
+        sys.exit(0)
+    if "--topk" in sys.argv:
+        make_tiny_topk()
         sys.exit(0)
     make_ngram()
     if "--skip-decoder" not in sys.argv:

@@ -14,7 +14,7 @@
 import numpy as np
 import pytest
 
-from conftest import GOLDEN  # noqa: F401  (conftest registers the marker)
+from conftest import GOLDEN
 from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_turn, specstream
 from paper_2506_15556_b200.shapes import TINY, small_shape
 from paper_2506_15556_b200.fused import verify_greedy, verify_topk
@@ -115,5 +115,27 @@ def test_topk_contract_errors():
             lm.verify_topk_detail([5, 6, 7], [8, 9], 0)
         with pytest.raises(ValueError):
             lm.verify_topk_detail([5, 6, 7], [lm.vocab_size + 3], 2)
+    finally:
+        lm.close()
+
+
+TOPK_TURNS = __import__("json").loads((GOLDEN / "tiny_topk_turns.json").read_text())
+
+
+@pytest.mark.parametrize("i", range(len(TOPK_TURNS["turns"])))
+def test_topk_turns_equal_reference_golden(i):
+    """Top-k (k = 3) turns pinned to the reference: tests/golden/tiny_topk_turns.json
+    holds the event logs the reference's run_turn produced with its own
+    verify_topk / topk_tokens on the float64 oracle decoder. The fused device
+    verifier (ranks counted on the device) reproduces every event — including
+    the accept-heavy rounds (k = 32, the whole candidate) whose first sentence
+    resumes from the buffered TTS job."""
+    rec = TOPK_TURNS["turns"][i]
+    cfg = PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32, verifier="topk", topk_k=3)
+    lm = B200LM(TINY, seed=TOPK_TURNS["seed"], max_seq=1024)
+    try:
+        res = run_turn([], make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+        assert res.final_text == rec["speculative"]["final_text"]
+        assert [e.to_dict() for e in res.events] == rec["speculative"]["events"]
     finally:
         lm.close()

@@ -14,7 +14,7 @@ from __future__ import annotations
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path.cwd()) if (Path.cwd() / "paper_2506_15556_b200").exists() else str(Path(__file__).resolve().parents[1]))
 
 import numpy as np  # noqa: E402
 
