@@ -112,6 +112,9 @@ struct TmaDesc {
 };
 bool encode_tma_2d_bf16(TmaDesc* out, const void* base, uint64_t inner, uint64_t outer,
                         uint32_t box_inner, uint32_t box_outer);
+bool encode_tma_2d_f32(TmaDesc* out, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                       uint32_t box_outer);
+constexpr int kXBoxRows = 8;  // rows per residual-row box of the wide finalisation
 
 constexpr int kTileTc = 128;
 
@@ -127,6 +130,7 @@ struct MegaParams {
   float eps, attn_scale;
   const CUtensorMap* wmaps; // [4L + 1] device-resident tensor maps
   const CUtensorMap* xmaps; // [4] activation maps for this ntok: xb, attn, act, hn
+  const CUtensorMap* xrows; // fp32 residual x [kMaxWindow][H], boxes of 128 features x kXBoxRows rows
   int* tokens_dev;
   int* argmax_pos;
   const __nv_bfloat16* embed;

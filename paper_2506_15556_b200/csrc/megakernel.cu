@@ -1181,8 +1181,12 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
   const bool has_rope = kind == PH_QKV;
   const int hd = P.hd, half = hd >> 1;
   const int rope_row = half * 2;  // floats per RoPE row (cos, sin pairs)
-  const int per_row = np * 128 + (has_x ? 128 : has_rope ? rope_row : 0);
-  const int batch = cap_floats / per_row;  // >= 8 rows
+  // staged per row: the pieces' partials, and for O/D the residual row (its
+  // boxes are kXBoxRows rows, so the residual area is padded to a multiple);
+  // QKV's RoPE (cos, sin) is read straight from the (L1-cached) table
+  const int per_row = np * 128 + (has_x ? 128 : 0);
+  const int batch = has_x ? (cap_floats - kXBoxRows * 128) / per_row / kXBoxRows * kXBoxRows  // >= 8 rows
+                          : cap_floats / per_row;
   const int f0 = 4 * lane;               // this thread's first feature within the tile
   for (int b0 = T.r_lo; b0 < T.r_hi; b0 += batch) {
     const int nb = min(batch, T.r_hi - b0);
@@ -1190,15 +1194,14 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
     if (tid == 0) {
       fence_proxy_async_global();  // generic writes of other CTAs (acquired) -> async-proxy reads
       if (trace_p >= 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 10);
-      const uint32_t bytes = uint32_t(np * nb * 512 + (has_x ? nb * 512 : has_rope ? nb * rope_row * 4 : 0));
+      const int xboxes = has_x ? (nb + kXBoxRows - 1) / kXBoxRows : 0;
+      const uint32_t bytes = uint32_t(np * nb * 512 + xboxes * kXBoxRows * 512);
       mbar_expect_tx(wbar, bytes);
       for (int pc = 0; pc < np; ++pc)
         bulk_g2s(smem_u32(S + pc * nb * 128),
                  P.part + piece_off_slot(T.c_first + pc, pc == 0 ? T.slot0 : 0, 0) + size_t(b0) * 128, nb * 512, wbar);
-      if (has_x)
-        for (int r = 0; r < nb; ++r) bulk_g2s(smem_u32(X + r * 128), P.x + size_t(b0 + r) * P.H + T.tile * 128, 512, wbar);
-      else if (has_rope)
-        bulk_g2s(smem_u32(X), P.rope + size_t(n0 + b0) * half, uint32_t(nb * rope_row * 4), wbar);
+      for (int j = 0; j < xboxes; ++j)  // residual rows b0 + 8j .., 128 features of the tile
+        tma_load_2d(smem_u32(X + j * kXBoxRows * 128), P.xrows, wbar, T.tile * 128, b0 + j * kXBoxRows);
       if (trace_p >= 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 3);
     }
     mbar_wait(wbar, wphase);
@@ -1214,7 +1217,8 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
         acc.z += o.z;
         acc.w += o.w;
       }
-      vec_finish_row(P, kind, layer, n0, w, lane, T.tile, t, acc, X + r * (has_x ? 128 : rope_row), es);
+      const float* xin = has_x ? X + r * 128 : reinterpret_cast<const float*>(P.rope) + size_t(n0 + t) * rope_row;
+      vec_finish_row(P, kind, layer, n0, w, lane, T.tile, t, acc, xin, es);
     }
     if (trace_p >= 0 && tid == 0 && b0 == T.r_lo) stamp(P, trace_p, blockIdx.x, gridDim.x, 15);
     wk_bar();  // the staging area is reused by the next batch / tile

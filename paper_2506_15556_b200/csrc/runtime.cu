@@ -462,6 +462,7 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.attn_scale = float(1.0 / std::sqrt(double(h->hd)));
   P.wmaps = h->d_wmaps;
   P.xmaps = h->d_xmaps + size_t(ntok / 16 - 1) * 4;
+  P.xrows = h->d_xmaps + size_t(kMaxWindow / 16) * 4;
   P.tokens_dev = h->tokens_dev;
   P.argmax_pos = h->argmax_pos;
   P.embed = static_cast<const bf*>(h->embed);
@@ -919,7 +920,7 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     h->mega_cnt_words = 64 + size_t(3 + 5 * h->L) * h->mega_max_tiles;
     h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
-    h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4);
+    h->d_xmaps = h->dalloc<CUtensorMap>(size_t(kMaxWindow / 16) * 4 + 1);  // + the fp32 residual-row map
     if (!h->mega_part || !h->mega_tags || !h->mega_epoch || !h->mega_cnt || !h->d_wmaps || !h->d_xmaps) return bad("megakernel buffers");
     if (const char* tr = std::getenv("PS_TRACE"); tr && tr[0] == '1')
       h->mega_trace = h->dalloc<unsigned long long>(size_t(3 + 5 * h->L) * h->sms * 16);
@@ -932,7 +933,13 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     }
     std::memcpy(&wm[4 * h->L], h->tm_head.bytes, sizeof(CUtensorMap));
     if (copy_sync(h, h->d_wmaps, wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice) != cudaSuccess) return (ps_destroy(h), fail(PS_ERR_CUDA, "initial upload failed"));
-    std::vector<CUtensorMap> xm(size_t(kMaxWindow / 16) * 4);
+    std::vector<CUtensorMap> xm(size_t(kMaxWindow / 16) * 4 + 1);
+    {
+      TmaDesc xr;
+      if (!encode_tma_2d_f32(&xr, h->x, h->H, kMaxWindow, 128, kXBoxRows))
+        return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
+      std::memcpy(&xm[size_t(kMaxWindow / 16) * 4], xr.bytes, sizeof(CUtensorMap));
+    }
     for (int k = 0; k < kMaxWindow / 16; ++k) {
       const ActDescs* ad = act_descs(h, 16 * (k + 1));
       if (!ad) return (ps_destroy(h), fail(PS_ERR_CUDA, "TMA descriptor encode failed"));
