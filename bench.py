@@ -223,9 +223,9 @@ def load_schedule(shape_name: str) -> dict:
 
 
 def summarize_schedule(entries) -> list:
-    """[(ctx, rows)] of one conversation -> [n_passes, rows, decode_passes, extend_passes]."""
-    rows = sum(r for _, r in entries)
-    dec = sum(1 for _, r in entries if r == 1)
+    """[(ctx, rows, ...)] of one conversation -> [n_passes, rows, decode_passes, extend_passes]."""
+    rows = sum(e[1] for e in entries)
+    dec = sum(1 for e in entries if e[1] == 1)
     return [len(entries), rows, dec, len(entries) - dec]
 
 
@@ -319,6 +319,7 @@ def main(argv=None):
     cfg = c5_config(lm.vocab, spec)
     per = args.conv_per_step
     live_sched: dict = {}
+    traffic = {"bytes": 0.0, "ms": 0.0, "decode_bytes": 0.0, "decode_ms": 0.0}
 
     def barrier():
         if world > 1:
@@ -333,12 +334,21 @@ def main(argv=None):
             lm.schedule = []
             run_conversation(conv.turns, cfg, lm, conversation_id=conv.id)
             live_sched[conv.id] = summarize_schedule(lm.schedule)
+            for ctx_len, rows, ms in lm.schedule:
+                b = shape.pass_bytes(rows, ctx_len)
+                traffic["bytes"] += b
+                traffic["ms"] += ms
+                if rows == 1:
+                    traffic["decode_bytes"] += b
+                    traffic["decode_ms"] += ms
             n += 1
         lm.schedule = None
         return n
 
     for w in range(args.warmup):
         run_step(w)
+    for k in traffic:
+        traffic[k] = 0.0
     s0 = lm.stats()
     sampler = ClockSampler(local)
     barrier()
@@ -401,6 +411,12 @@ def main(argv=None):
                 "h2d_bytes_per_step": delta["h2d_bytes"] / args.steps,
                 "d2h_bytes_per_step": delta["d2h_bytes"] / args.steps},
         "schedule": sched_info,
+        # every timed pass's algorithmic bytes (weights + cached KV read + new KV
+        # written + embedding rows) over its own device time: the whole workload's HBM roofline
+        "workload_hbm": {"algorithmic_bytes": traffic["bytes"], "device_ms": traffic["ms"],
+                         "achieved_GBs": traffic["bytes"] / max(traffic["ms"], 1e-9) / 1e6,
+                         "frac": traffic["bytes"] / max(traffic["ms"], 1e-9) / 1e6 / hbm,
+                         "decode_frac": traffic["decode_bytes"] / max(traffic["decode_ms"], 1e-9) / 1e6 / hbm},
         "gpu_launches": delta["launches"], "passes": delta["passes"], "rows_computed": delta["rows"],
         "clocks": clocks,
     }

@@ -175,7 +175,7 @@ class B200LM(_lm.LanguageModel):
         self.verify_ms: list[float] = []
         self.decode_ms: list[float] = []   # device ms of every 1-row pass
         self.extend_ms: list[tuple] = []   # (rows, device ms) of every wider pass
-        # (context length, rows computed) of every pass, when a caller sets it to a list
+        # (context length, rows computed, device ms) of every pass, when a caller sets it to a list
         self.schedule: list | None = None
 
     # -- plumbing -----------------------------------------------------------------
@@ -205,11 +205,11 @@ class B200LM(_lm.LanguageModel):
         self._call("ps_get_stats", ctypes.byref(st))
         return int(st.rows)
 
-    def _note_verify_pass(self, n_ctx: int, rows_before: int) -> None:
+    def _note_verify_pass(self, n_ctx: int, rows_before: int, ms: float) -> None:
         if self.schedule is not None:
             rows = self._rows_computed() - rows_before
             if rows:
-                self.schedule.append((n_ctx, rows))
+                self.schedule.append((n_ctx, rows, ms))
 
     def resident(self) -> list[int]:
         n = ctypes.c_int32()
@@ -282,7 +282,7 @@ class B200LM(_lm.LanguageModel):
         ctx = tuple(int(t) for t in context)
         argmax, computed, ms = self._sync(list(ctx), start)
         if computed and self.schedule is not None:
-            self.schedule.append((len(ctx), computed))
+            self.schedule.append((len(ctx), computed, ms))
         if computed == 1:
             self.decode_ms.append(ms)
         elif computed > 1:
@@ -310,7 +310,7 @@ class B200LM(_lm.LanguageModel):
         rows0 = self._rows_computed() if self.schedule is not None else 0
         self._call("ps_verify_greedy", p, len(prompt), c, len(candidate), ctypes.byref(k), ctypes.byref(term),
                    None, ctypes.byref(ms))
-        self._note_verify_pass(len(prompt) + len(candidate), rows0)
+        self._note_verify_pass(len(prompt) + len(candidate), rows0, ms.value)
         self.last_verify_ms = ms.value
         self.verify_ms.append(ms.value)
         seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)
@@ -332,7 +332,7 @@ class B200LM(_lm.LanguageModel):
             raise ValueError("verification requires a nonempty prompt context")
         rows0 = self._rows_computed() if self.schedule is not None else 0
         d = self.verify_topk_detail(prompt, candidate, topk)
-        self._note_verify_pass(len(prompt) + len(candidate), rows0)
+        self._note_verify_pass(len(prompt) + len(candidate), rows0, d["gpu_ms"])
         self.last_verify_ms = d["gpu_ms"]
         self.verify_ms.append(d["gpu_ms"])
         seq = tuple(int(t) for t in prompt) + tuple(int(t) for t in candidate)

@@ -89,6 +89,13 @@ class DecoderShape:
     def kv_bytes_per_token(self) -> int:
         return self.layers * 2 * self.kv_dim * self.elem_bytes
 
+    def pass_bytes(self, rows: int, ctx: int) -> int:
+        """Algorithmic HBM bytes of one pass computing `rows` new positions of a
+        `ctx`-token sequence: weights once, the KV of every position
+        the attention reads (cached and new), the new KV written, the embedding rows."""
+        kv = self.kv_bytes_per_token()
+        return self.weight_bytes_per_pass() + ctx * kv + rows * kv + rows * self.hidden * self.elem_bytes
+
     def as_dict(self) -> dict:
         return asdict(self)
 

@@ -56,3 +56,12 @@ def test_both_arms_print_the_same_config():
     assert cfg["timed_conversation_ids"] == [24, 64]
     assert bench.workload_config(bench.parse(["--impl", "reference", "--steps", "5", "--warmup", "3",
                                               "--conv-per-step", "2"]), world=4) == cfg
+
+
+def test_pass_bytes_match_survey_floors():
+    from paper_2506_15556_b200.shapes import LLAMA3_8B, QWEN_05B
+    # c3 decode (W=1, C=512) 15.077 GB, c3 verify (W=72, C=128) 15.046 GB,
+    # c2 verify (W=72) 1.983 GB
+    assert LLAMA3_8B.pass_bytes(1, 513) / 1e9 == pytest.approx(15.077, abs=2e-3)
+    assert LLAMA3_8B.pass_bytes(72, 200) / 1e9 == pytest.approx(15.046, abs=2e-3)
+    assert QWEN_05B.pass_bytes(72, 200) / 1e9 == pytest.approx(1.983, abs=2e-3)
