@@ -6,6 +6,7 @@
 // fixed by (n, K-split) alone: a row scored in a 72-row verify pass is
 // bit-identical to the same row scored by a 1-row decode pass.
 #include "common.cuh"
+#include "f32_math.cuh"
 #include "kernels.h"
 
 namespace ps {

@@ -10,6 +10,7 @@
 // combines them in order. A row computed inside a 72-row verify pass is
 // therefore bit-identical to the same row computed by a 1-row decode step.
 #include "common.cuh"
+#include "f32_math.cuh"
 #include "kernels.h"
 
 namespace ps {
@@ -52,9 +53,9 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(PassCtx* ctx, const int
     ss = fmaf(v, v, ss);
   }
   ss = block_sum<256>(ss, red);
-  const float rstd = 1.0f / sqrtf(ss / float(H) + eps);
+  const float rstd = f32_rstd(ss, H, eps);
   T* o = xn + size_t(t) * H;
-  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(xr[c] * rstd);
+  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(__fmul_rn(xr[c], rstd));
 }
 
 template <typename T>
@@ -84,8 +85,7 @@ __global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __rest
   const size_t sstride = size_t(kMaxWindow) * N;
   const float* pr = part + size_t(t) * N;
   auto sum_col = [&](int c) {
-    float v = pr[c];
-    for (int s = 1; s < splits; ++s) v += pr[s * sstride + c];
+    float v = f32_sum_splits(pr + c, splits, sstride);  // split order, loads in flight together
     if (bias) v += ld_as_f32(bias + c);
     return v;
   };
@@ -99,9 +99,8 @@ __global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __rest
       const int h = pp / half, i = pp % half;
       const int col = (is_q ? 0 : heads * hd) + h * hd + i;
       const float a = sum_col(col), b = sum_col(col + half);
-      const float2 cs = rope[size_t(pos) * half + i];
-      const float ra = a * cs.x - b * cs.y;
-      const float rb = b * cs.x + a * cs.y;
+      float ra, rb;
+      f32_rope(a, b, rope[size_t(pos) * half + i], ra, rb);
       if (is_q) {
         T* qr = q + size_t(t) * heads * hd + h * hd;
         qr[i] = from_f32<T>(ra);
@@ -153,48 +152,44 @@ __global__ void attention_page_kernel(const PassCtx* __restrict__ ctx, const T* 
   float* Qs = Vs + kPage * hd;          // [grp][hd]
   const size_t page = size_t(page_table[s]);
   const size_t off = size_t(layer) * g.layer_stride() + (page * g.kv_heads + kvh) * kPage * hd;
-  for (int e = threadIdx.x; e < nkeys * hd; e += blockDim.x) {
-    const int j = e / hd, d = e % hd;
-    Ks[j * (hd + 1) + d] = ld_as_f32(kpool + off + e);
-    Vs[j * hd + d] = ld_as_f32(vpool + off + e);
+  if constexpr (sizeof(T) == 4) {
+    // float4 loads, four in flight per thread for K and for V (hd is a multiple of 4)
+    const int n4 = nkeys * hd / 4;
+    for (int e0 = threadIdx.x; e0 < n4; e0 += blockDim.x * 4) {
+      float4 kv[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + int(blockDim.x) * u;
+        if (e < n4) {
+          kv[u] = __ldg(reinterpret_cast<const float4*>(kpool + off) + e);
+          vv[u] = __ldg(reinterpret_cast<const float4*>(vpool + off) + e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + int(blockDim.x) * u;
+        if (e < n4) {
+          const int j = (4 * e) / hd, d = (4 * e) % hd;
+          float* kr = Ks + j * (hd + 1) + d;
+          kr[0] = kv[u].x; kr[1] = kv[u].y; kr[2] = kv[u].z; kr[3] = kv[u].w;
+          *reinterpret_cast<float4*>(Vs + j * hd + d) = vv[u];
+        }
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < nkeys * hd; e += blockDim.x) {
+      const int j = e / hd, d = e % hd;
+      Ks[j * (hd + 1) + d] = ld_as_f32(kpool + off + e);
+      Vs[j * hd + d] = ld_as_f32(vpool + off + e);
+    }
   }
   const T* qrow = q + size_t(t) * heads * hd + size_t(kvh) * grp * hd;
   for (int e = threadIdx.x; e < grp * hd; e += blockDim.x) Qs[e] = ld_as_f32(qrow + e);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w >= grp) return;
-  const float* qs = Qs + w * hd;
-  float sc[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int j = lane + 32 * r;
-    float acc = 0.f;
-    if (j < nkeys) {
-      const float* kr = Ks + j * (hd + 1);
-      for (int d = 0; d < hd; ++d) acc = fmaf(qs[d], kr[d], acc);
-      sc[r] = acc * scale;
-    } else {
-      sc[r] = -INFINITY;
-    }
-  }
-  const float m = warp_max(fmaxf(sc[0], sc[1]));
-  const float p0 = (lane < nkeys) ? expf(sc[0] - m) : 0.f;
-  const float p1 = (lane + 32 < nkeys) ? expf(sc[1] - m) : 0.f;
-  const float l = warp_sum(p0 + p1);
-  const int h = kvh * grp + w;
-  const size_t slot = (size_t(t) * heads + h) * max_splits + s;
-  for (int d = lane; d < hd; d += 32) {
-    float acc = 0.f;
-    for (int j = 0; j < nkeys; ++j) {
-      const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
-      acc = fmaf(pj, Vs[j * hd + d], acc);
-    }
-    o_part[slot * hd + d] = acc;
-  }
-  if (lane == 0) {
-    ml_part[slot * 2] = m;
-    ml_part[slot * 2 + 1] = l;
-  }
+  const size_t slot = (size_t(t) * heads + kvh * grp + w) * max_splits + s;
+  f32_attn_page_head(Qs + w * hd, Ks, Vs, hd, nkeys, scale, lane, o_part + slot * hd, ml_part + slot * 2);
 }
 
 template <typename T>
@@ -206,15 +201,7 @@ __global__ void attention_combine_kernel(const PassCtx* __restrict__ ctx, int he
   if (ctx->stop || t >= ctx->rows) return;
   const int nsplit = (ctx->n0 + t) / kPage + 1;
   const size_t base = (size_t(t) * heads + h) * max_splits;
-  float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ml_part[(base + s) * 2]);
-  float L = 0.f, acc = 0.f;
-  for (int s = 0; s < nsplit; ++s) {
-    const float f = expf(ml_part[(base + s) * 2] - M);
-    L = fmaf(ml_part[(base + s) * 2 + 1], f, L);
-    acc = fmaf(o_part[(base + s) * hd + d], f, acc);
-  }
-  out[size_t(t) * heads * hd + size_t(h) * hd + d] = from_f32<T>(acc / L);
+  out[size_t(t) * heads * hd + size_t(h) * hd + d] = from_f32<T>(f32_attn_combine(o_part, ml_part, base, nsplit, hd, d));
 }
 
 template <typename T>
@@ -256,16 +243,15 @@ __global__ void __launch_bounds__(256) residual_norm_kernel(const PassCtx* __res
   const float* pr = part + size_t(t) * H;
   float ss = 0.f;
   for (int c = threadIdx.x; c < H; c += 256) {
-    float d = pr[c];
-    for (int s = 1; s < splits; ++s) d += pr[s * sstride + c];
-    const float v = xr[c] + d;
+    const float d = f32_sum_splits(pr + c, splits, sstride);
+    const float v = __fadd_rn(xr[c], d);
     xr[c] = v;
     ss = fmaf(v, v, ss);
   }
   ss = block_sum<256>(ss, red);
-  const float rstd = 1.0f / sqrtf(ss / float(H) + eps);
+  const float rstd = f32_rstd(ss, H, eps);
   T* o = hn_cache ? hn_cache + size_t(ctx->n0 + t) * H : xn + size_t(t) * H;
-  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(xr[c] * rstd);
+  for (int c = threadIdx.x; c < H; c += 256) o[c] = from_f32<T>(__fmul_rn(xr[c], rstd));
 }
 
 template <typename T>
@@ -287,13 +273,8 @@ __global__ void swiglu_kernel(const PassCtx* __restrict__ ctx, const float* __re
   const int N = 2 * I;
   const size_t sstride = size_t(kMaxWindow) * N;
   const float* pr = part + size_t(t) * N;
-  float gsum = pr[i], usum = pr[I + i];
-  for (int s = 1; s < splits; ++s) {
-    gsum += pr[s * sstride + i];
-    usum += pr[s * sstride + I + i];
-  }
-  const float silu = gsum / (1.0f + expf(-gsum));
-  act[size_t(t) * I + i] = from_f32<T>(silu * usum);
+  const float gsum = f32_sum_splits(pr + i, splits, sstride), usum = f32_sum_splits(pr + I + i, splits, sstride);
+  act[size_t(t) * I + i] = from_f32<T>(f32_swiglu(gsum, usum));
 }
 
 template <typename T>
