@@ -165,49 +165,63 @@ def cpu_model() -> str:
 
 # -- CPU pricing of a pass schedule ---------------------------------------------------------
 
-def cpu_pass_model(shape, sample_s: float, threads: int, context: int = 128,
-                   widths=(1, 8, 32, 72)) -> dict:
-    """Oracle decoder (numpy fp32, BLAS on `threads` host threads) per-pass times at `shape`:
-    t_decode = the median 1-row pass, and t(rows) = a + b*rows for wider passes (least
-    squares over the per-width medians of the wider widths).
+class CpuPassTimer:
+    """Oracle decoder (numpy fp32, BLAS on all host threads) at `shape`, built once.
 
-    Every layer streams layer 0's weights (share_layer_weights): the same bytes and FLOPs
-    per pass as the full model, without generating 8B values on the host. Passes run over
-    a `context`-token resident prefix (attention is < 1% of a CPU pass at this length)."""
-    import numpy as np
-    from oracle.decoder import DecoderOracle
+    Every layer streams layer 0's weights (share_layer_weights): the same bytes and
+    FLOPs per pass as the full model, without generating 8B values on the host.
+    Passes run over a `context`-token resident prefix (attention is < 1% of a CPU
+    pass at this length)."""
 
-    t0 = time.perf_counter()
-    d = dict(shape.as_dict())
-    d["mode"] = 0  # fp32 arithmetic: no bf16 rounding emulation in the timed port
-    m = DecoderOracle(d, seed=0, dtype=np.float32, share_layer_weights=True)
-    rng = np.random.default_rng(0)
-    m.extend([int(t) for t in rng.integers(4, shape.vocab, context)])
-    setup_s = time.perf_counter() - t0
-    samples = {w: [] for w in widths}
-    deadline = time.perf_counter() + sample_s
-    i = 0
-    while time.perf_counter() < deadline or any(len(v) < 2 for v in samples.values()):
-        w = widths[i % len(widths)]
-        i += 1
-        m.truncate(context)
-        t = time.perf_counter()
-        m.extend([int(x) for x in rng.integers(4, shape.vocab, w)])
-        samples[w].append((time.perf_counter() - t) * 1e3)
-        if w == 1:  # decode passes are the bulk of a schedule: sample them more densely
-            for _ in range(3):
-                t = time.perf_counter()
-                m.extend([int(rng.integers(4, shape.vocab))])
-                samples[1].append((time.perf_counter() - t) * 1e3)
-        if i > 400:
-            break
-    ys = {w: statistics.median(samples[w]) for w in widths}
-    wide = [w for w in widths if w > 1]
-    b, a = np.polyfit(np.array(wide, dtype=np.float64), np.array([ys[w] for w in wide]), 1)
-    return {"decode_ms": float(ys[1]), "a_ms": float(a), "b_ms_per_row": float(b),
-            "median_ms": {str(w): float(y) for w, y in ys.items()},
-            "samples": {str(w): len(v) for w, v in samples.items()}, "setup_s": setup_s, "threads": threads,
-            "context": context}
+    WIDTHS = (1, 8, 32, 72)
+
+    def __init__(self, shape, threads: int, context: int = 128):
+        import numpy as np
+        from oracle.decoder import DecoderOracle
+
+        t0 = time.perf_counter()
+        d = dict(shape.as_dict())
+        d["mode"] = 0  # fp32 arithmetic: no bf16 rounding emulation in the timed port
+        self.m = DecoderOracle(d, seed=0, dtype=np.float32, share_layer_weights=True)
+        self.rng = np.random.default_rng(0)
+        self.vocab, self.context, self.threads = shape.vocab, context, threads
+        self.m.extend([int(t) for t in self.rng.integers(4, shape.vocab, context)])
+        self.setup_s = time.perf_counter() - t0
+
+    def sample(self, sample_s: float) -> dict:
+        """Median pass times: t_decode = the 1-row pass, t(rows) = a + b*rows for wider
+        passes (least squares over the per-width medians)."""
+        import numpy as np
+
+        m, rng, widths = self.m, self.rng, self.WIDTHS
+        samples = {w: [] for w in widths}
+        deadline = time.perf_counter() + sample_s
+        i = 0
+        while time.perf_counter() < deadline or any(len(v) < 2 for v in samples.values()):
+            w = widths[i % len(widths)]
+            i += 1
+            m.truncate(self.context)
+            t = time.perf_counter()
+            m.extend([int(x) for x in rng.integers(4, self.vocab, w)])
+            samples[w].append((time.perf_counter() - t) * 1e3)
+            if w == 1:  # decode passes are the bulk of a schedule: sample them more densely
+                for _ in range(3):
+                    t = time.perf_counter()
+                    m.extend([int(rng.integers(4, self.vocab))])
+                    samples[1].append((time.perf_counter() - t) * 1e3)
+            if i > 400:
+                break
+        ys = {w: statistics.median(samples[w]) for w in widths}
+        wide = [w for w in widths if w > 1]
+        b, a = np.polyfit(np.array(wide, dtype=np.float64), np.array([ys[w] for w in wide]), 1)
+        return {"decode_ms": float(ys[1]), "a_ms": float(a), "b_ms_per_row": float(b),
+                "median_ms": {str(w): float(y) for w, y in ys.items()},
+                "samples": {str(w): len(v) for w, v in samples.items()}, "setup_s": self.setup_s,
+                "threads": self.threads, "context": self.context}
+
+
+def cpu_pass_model(shape, sample_s: float, threads: int, context: int = 128) -> dict:
+    return CpuPassTimer(shape, threads, context).sample(sample_s)
 
 
 def cpu_schedule_ms(model: dict, entries) -> float:
@@ -266,10 +280,11 @@ def reference_arm(args):
     if not have:
         print(json.dumps({"impl": "reference", "unavailable": f"no committed pass schedule for {args.shape}"}))
         return
-    per_step = max(2.0, args.cpu_sample_s / max(1, args.steps + args.warmup))
+    per_step = max(2.0, args.cpu_sample_s / max(1, args.steps))
+    timer = CpuPassTimer(shape, threads)  # built once: the oracle's weights are the setup cost
     models = []
     for i in range(args.warmup + args.steps):
-        m = cpu_pass_model(shape, per_step if i >= args.warmup else 1.0, threads)
+        m = timer.sample(per_step if i >= args.warmup else 1.0)
         if i >= args.warmup:
             models.append(m)
     model = {k: statistics.median(m[k] for m in models) for k in ("decode_ms", "a_ms", "b_ms_per_row")}
