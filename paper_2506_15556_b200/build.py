@@ -50,11 +50,18 @@ def _digest() -> str:
     return h.hexdigest()
 
 
+LAST = {"compiled": False, "digest": ""}
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile when the sources, headers or flags changed (sha256 stamp); LAST records
+    whether this call compiled or reused a library built from identical sources."""
     stamp = PKG / "_build" / "stamp"
     digest = _digest()
+    LAST.update(compiled=False, digest=digest[:16])
     if LIB.exists() and stamp.exists() and stamp.read_text() == digest and not force:
         return LIB
+    LAST["compiled"] = True
     OBJ.mkdir(exist_ok=True)
     cc = nvcc()
 
