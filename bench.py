@@ -502,6 +502,10 @@ def main(argv=None):
                        f"summed over this run's pass schedule ({len(mine)} conversations)"),
             "per_pass_ms": model["median_ms"],
         }
+        dec, ver = line.get("decode_step_ms", {}).get("p50"), line.get("verify_step_ms", {}).get("p50")
+        if dec and ver:  # same pass shapes on both sides: 1-row decode, 72-row verify window
+            line["cpu_baseline"]["per_pass_gpu_speedup"] = {"decode_1_row": model["median_ms"]["1"] / dec,
+                                                            "verify_72_rows": model["median_ms"]["72"] / ver}
     if rank == 0:
         print(json.dumps(line), flush=True)
     lm.close()
