@@ -177,6 +177,9 @@ class B200LM(_lm.LanguageModel):
         self.extend_ms: list[tuple] = []   # (rows, device ms) of every wider pass
         # (context length, rows computed, device ms) of every pass, when a caller sets it to a list
         self.schedule: list | None = None
+        # the same for every call (a prefix hit logs 0 rows): report.annotate_events joins it
+        # with the reference's verify / generate_step events
+        self.call_log: list | None = None
 
     # -- plumbing -----------------------------------------------------------------
     def _call(self, name: str, *args) -> None:
@@ -206,10 +209,12 @@ class B200LM(_lm.LanguageModel):
         return int(st.rows)
 
     def _note_verify_pass(self, n_ctx: int, rows_before: int, ms: float) -> None:
-        if self.schedule is not None:
+        if self.schedule is not None or self.call_log is not None:
             rows = self._rows_computed() - rows_before
-            if rows:
+            if rows and self.schedule is not None:
                 self.schedule.append((n_ctx, rows, ms))
+            if self.call_log is not None:
+                self.call_log.append((n_ctx, rows, ms))
 
     def resident(self) -> list[int]:
         n = ctypes.c_int32()
@@ -283,6 +288,8 @@ class B200LM(_lm.LanguageModel):
         argmax, computed, ms = self._sync(list(ctx), start)
         if computed and self.schedule is not None:
             self.schedule.append((len(ctx), computed, ms))
+        if self.call_log is not None:
+            self.call_log.append((len(ctx), computed, ms))
         if computed == 1:
             self.decode_ms.append(ms)
         elif computed > 1:
@@ -307,7 +314,7 @@ class B200LM(_lm.LanguageModel):
         k = ctypes.c_int32()
         term = ctypes.c_int32()
         ms = ctypes.c_float()
-        rows0 = self._rows_computed() if self.schedule is not None else 0
+        rows0 = self._rows_computed() if self.schedule is not None or self.call_log is not None else 0
         self._call("ps_verify_greedy", p, len(prompt), c, len(candidate), ctypes.byref(k), ctypes.byref(term),
                    None, ctypes.byref(ms))
         self._note_verify_pass(len(prompt) + len(candidate), rows0, ms.value)
@@ -330,7 +337,7 @@ class B200LM(_lm.LanguageModel):
         """Fused top-k verify (rank counting on the device): (k, handle over prompt ++ candidate, cost)."""
         if not prompt:
             raise ValueError("verification requires a nonempty prompt context")
-        rows0 = self._rows_computed() if self.schedule is not None else 0
+        rows0 = self._rows_computed() if self.schedule is not None or self.call_log is not None else 0
         d = self.verify_topk_detail(prompt, candidate, topk)
         self._note_verify_pass(len(prompt) + len(candidate), rows0, d["gpu_ms"])
         self.last_verify_ms = d["gpu_ms"]

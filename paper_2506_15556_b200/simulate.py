@@ -37,7 +37,7 @@ from pathlib import Path
 
 from ._specstream import specstream
 from .fused import run_conversation
-from .report import summarize_percentiles
+from .report import annotate_events, summarize_percentiles
 
 _queue_ids = itertools.count()
 
@@ -66,18 +66,31 @@ class ConversationQueue:
 
 
 def run_sharded(conversations, cfg, lm, out_dir, rank: int = 0, world: int = 1, baseline: bool = False,
-                group=None, queue: ConversationQueue | None = None) -> list[dict]:
+                group=None, queue: ConversationQueue | None = None, annotate: bool = False) -> list[dict]:
     """Simulate the conversations this rank claims, write their event logs; rank 0 writes the report.
 
+    annotate: a B200LM backend's per-call device time, rows and algorithmic bytes are added
+    to every verify / generate_step event (report.annotate_events; greedy / top-k only).
     Returns the per-turn metrics (all ranks' on rank 0, this rank's elsewhere)."""
     out = Path(out_dir)
     queue = queue if queue is not None else ConversationQueue(len(conversations), world)
     recs = []
+    trace = annotate and getattr(lm, "call_log", "absent") is None and getattr(lm, "shape", None) is not None
     while (i := queue.claim()) is not None:
         conv = conversations[i]
-        for res in run_conversation(conv.turns, cfg, lm, conversation_id=conv.id, baseline=baseline):
+        if trace:
+            lm.call_log = []
+        results = run_conversation(conv.turns, cfg, lm, conversation_id=conv.id, baseline=baseline)
+        calls = lm.call_log if trace else None
+        if trace:
+            lm.call_log = None
+        for res in results:
+            events = res.events
+            if trace:  # this turn's share of the conversation's backend calls, in order
+                n = sum(1 for e in events if e.kind in ("verify", "generate_step"))
+                events, calls = annotate_events(events, calls[:n], lm.shape), calls[n:]
             m = specstream.compute_metrics(res.events)
-            specstream.write_events_jsonl(res.events, out / "events" / f"{conv.id}_{m.round}.jsonl")
+            specstream.write_events_jsonl(events, out / "events" / f"{conv.id}_{m.round}.jsonl")
             recs.append((i, dataclasses.asdict(m)))
     if world > 1:
         import torch.distributed as dist
@@ -108,6 +121,7 @@ def main(argv=None) -> int:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cost-mode", default="modeled", choices=["modeled", "measured"])
     ap.add_argument("--baseline", action="store_true")
+    ap.add_argument("--annotate", action="store_true", help="add gpu_ms / rows / algorithmic_bytes to events")
     ap.add_argument("--out", required=True)
     a = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -131,7 +145,7 @@ def main(argv=None) -> int:
     cfg = c5_config(vocab, spec)
     lm = B200LM(shape, seed=a.seed, device=local, cost_mode=a.cost_mode)
     try:
-        rows = run_sharded(convs, cfg, lm, a.out, rank, world, a.baseline)
+        rows = run_sharded(convs, cfg, lm, a.out, rank, world, a.baseline, annotate=a.annotate)
     finally:
         lm.close()
     if rank == 0:

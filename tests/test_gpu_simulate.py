@@ -73,3 +73,33 @@ def test_sharded_simulation_on_b200_is_world_size_independent(tmp_path):
     assert a.keys() == b.keys() and len(a) == len(rows) + 2
     for k in a:
         assert a[k] == b[k], k
+
+
+def test_annotated_events_carry_device_time_and_bytes(tmp_path):
+    """SURVEY §5 tracing keys: with measured cost, every verify / generate_step event's
+    gpu_ms is the cost the SimClock was charged, and algorithmic_bytes is the pass's
+    SURVEY §8d byte count (0 for a prefix hit)."""
+    import json
+
+    from paper_2506_15556_b200 import B200LM
+    from paper_2506_15556_b200.shapes import small_shape
+    from paper_2506_15556_b200.simulate import run_sharded
+    from paper_2506_15556_b200.workload import WorkloadSpec, c5_config, synthetic_conversations
+
+    shape = small_shape()
+    lm = B200LM(shape, seed=2, max_seq=1024, cost_mode="measured")
+    try:
+        spec = WorkloadSpec(conversations=2, mean_words=10.0, max_words=20, system_words=8, seed=5)
+        convs = synthetic_conversations(lm.vocab, spec)
+        run_sharded(convs, c5_config(lm.vocab, spec, max_response_tokens=12), lm, tmp_path, annotate=True)
+    finally:
+        lm.close()
+    n = 0
+    for f in sorted((tmp_path / "events").glob("*.jsonl")):
+        for line in f.read_text().splitlines():
+            e = json.loads(line)
+            if e["kind"] in ("verify", "generate_step"):
+                n += 1
+                assert abs(e["gpu_ms"] - e["cost_ms"]) < 1e-6
+                assert (e["algorithmic_bytes"] > shape.weight_bytes_per_pass()) == (e["rows_computed"] > 0)
+    assert n > 0

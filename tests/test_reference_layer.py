@@ -89,3 +89,23 @@ def test_percentiles():
         percentile([], 50)
     s = summarize_percentiles([m, m])
     assert s["p50_ttfs_ms"] == m.ttfs_ms and s["turns"] == 2
+
+
+def test_annotate_events_joins_calls_in_order():
+    from paper_2506_15556_b200.report import annotate_events
+    from paper_2506_15556_b200.shapes import TINY
+
+    case = NGRAM["cases"][0]
+    cfg, vocab = _vocab_for(case)
+    lm = specstream.NGramLM(vocab, seed=case["seed"], latency=cfg.lm_latency)
+    res = specstream.run_conversation(case["turns"][:1], cfg, lm)[0]
+    n = sum(1 for e in res.events if e.kind in ("verify", "generate_step"))
+    calls = [(10 + i, i % 3, 0.5 * i) for i in range(n)]
+    out = annotate_events(res.events, calls, TINY)
+    passes = [e for e in out if e.kind in ("verify", "generate_step")]
+    assert [(e.payload["rows_computed"], e.payload["gpu_ms"]) for e in passes] == [(r, ms) for _, r, ms in calls]
+    assert all((e.payload["algorithmic_bytes"] > 0) == (e.payload["rows_computed"] > 0) for e in passes)
+    assert [e.to_dict()["kind"] for e in out] == [e.kind for e in res.events]
+    assert "gpu_ms" not in res.events[0].payload  # the reference's events are not modified
+    with pytest.raises(ValueError):
+        annotate_events(res.events, calls[1:], TINY)
