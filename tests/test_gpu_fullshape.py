@@ -37,7 +37,7 @@ RATE = 0.97
 
 @pytest.fixture(scope="module", params=[LLAMA3_8B, MISTRAL_7B], ids=lambda s: s.name)
 def big(request):
-    lm = B200LM(request.param, seed=0, max_seq=1024)
+    lm = B200LM(request.param, seed=0, max_seq=2048)
     yield lm
     lm.close()
 
@@ -73,3 +73,41 @@ def test_fullshape_turn_lossless(big):
     pred = specstream.run_turn([], stream, cfg, big)
     base = specstream.run_baseline([], stream, cfg, big)
     assert pred.final_text == base.final_text
+
+
+def test_fullshape_long_context_decode_rows_bitwise(big):
+    """A 1500-token context (24 KV pages: the general attention merge and several
+    attention units per CTA at full shape): a 72-row verify pass's last rows are
+    bitwise the rows of 1-row passes."""
+    rng = np.random.default_rng(13)
+    toks = [int(t) for t in rng.integers(4, big.vocab_size, 1500)]
+    big.truncate(0)
+    _, h, _ = big.forward(toks[:1428])
+    block, _, _ = big.forward(toks, h)
+    wide = np.stack([np.asarray(block.row_for(p)) for p in range(1494, 1500)])
+    big.truncate(1494)
+    step = []
+    for n in range(1495, 1501):
+        b, _, _ = big.forward(toks[:n])
+        step.append(np.asarray(b.row_for(n - 1)))
+    assert np.array_equal(wide.view(np.uint32), np.stack(step).view(np.uint32))
+
+
+def test_fullshape_nccl_join_one_rank(big, monkeypatch):
+    """The c4 join at full shape with a 1-rank communicator: packed keys all-reduced
+    after every pass (eager and inside the decode graph) give the instance's own ids."""
+    import os
+
+    import nvidia.nccl
+
+    monkeypatch.setenv("PS_NCCL_LIB", os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2"))
+    rng = np.random.default_rng(17)
+    toks = [int(t) for t in rng.integers(4, big.vocab_size, 96)]
+    big.truncate(0)
+    want = [t for t, _ in big.decode_greedy_fused(toks, 8)]
+    joined = B200LM(big.shape, seed=0, max_seq=1024)
+    try:
+        joined.init_shard_comm(B200LM.nccl_unique_id(), 0, 1)
+        assert [t for t, _ in joined.decode_greedy_fused(toks, 8)] == want
+    finally:
+        joined.close()
