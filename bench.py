@@ -69,6 +69,7 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-agreement", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c2 / c4-shape per-pass latencies")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     return ap.parse_args(argv)
 
@@ -241,6 +242,41 @@ def summarize_schedule(entries) -> list:
     rows = sum(e[1] for e in entries)
     dec = sum(1 for e in entries if e[1] == 1)
     return [len(entries), rows, dec, len(entries) - dec]
+
+
+def pass_latency(shape, hbm_gbs: float, ctx_len: int = 128, window: int = 72) -> dict:
+    """p50 device ms of 1-row decode steps and of `window`-row verify passes over a
+    `ctx_len`-token context at `shape`, each against its HBM floor (weights once)."""
+    import numpy as np
+    from paper_2506_15556_b200 import B200LM
+
+    lm = B200LM(shape, seed=0, max_seq=1024, cost_mode="measured")
+    try:
+        rng = np.random.default_rng(0)
+        ctx = [int(t) for t in rng.integers(4, shape.vocab, ctx_len)]
+        lm.decode_greedy_fused(ctx, 4)
+        dec = []
+        for _ in range(3):
+            lm.truncate(ctx_len)
+            dec += [c for _, c in lm.decode_greedy_fused(ctx, 24)[1:]]
+        cand = [int(t) for t in rng.integers(4, shape.vocab, window - 8)]
+        ver = []
+        for _ in range(5):
+            lm.truncate(ctx_len - 8)
+            ver.append(lm.verify_greedy_detail(ctx, cand)["gpu_ms"])
+    finally:
+        lm.close()
+    floor = shape.weight_bytes_per_pass() / (hbm_gbs * 1e9) * 1e3
+    # the verify window's matmul FLOPs against the dtype's arithmetic peak: bf16 = the measured
+    # cuBLAS sustained figure; fp32 = FFMA issue rate, 148 SMs x 128 lanes x 2 x 1.965 GHz (computed)
+    flops = 2.0 * window * (shape.body_params() + shape.head_params())
+    peak_tf = 1388.8 if shape.mode == 1 else 148 * 128 * 2 * 1.965e9 / 1e12
+    cfloor = flops / (peak_tf * 1e12) * 1e3
+    d, v = statistics.median(dec), statistics.median(ver)
+    return {"shape": shape.name, "dtype": "bf16" if shape.mode == 1 else "f32", "decode_step_ms": d,
+            "verify_step_ms": v, "window": window, "hbm_floor_ms": floor, "decode_roofline_frac": floor / d,
+            "verify_compute_floor_ms": cfloor, "verify_compute_peak_tflops": peak_tf,
+            "verify_roofline_frac": max(floor, cfloor) / v}
 
 
 def ttfs_roofline(results, pass_floor_ms: float) -> dict:
@@ -506,9 +542,14 @@ def main(argv=None):
         if dec and ver:  # same pass shapes on both sides: 1-row decode, 72-row verify window
             line["cpu_baseline"]["per_pass_gpu_speedup"] = {"decode_1_row": model["median_ms"]["1"] / dec,
                                                             "verify_72_rows": model["median_ms"]["72"] / ver}
+    lm.close()
+    if rank == 0 and world == 1 and not args.no_extra:
+        # the other BASELINE configs' per-pass latencies on this GPU (not part of `value`):
+        # c2 = Qwen2.5-0.5B shape in the fp32 bit-exact mode, c4 = Mistral-7B shape bf16
+        line["extra_configs"] = {name: pass_latency(SHAPES[key], hbm)
+                                 for name, key in (("c2", "qwen2.5-0.5b"), ("c4_one_gpu", "mistral-7b"))}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    lm.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
