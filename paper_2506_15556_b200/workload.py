@@ -1,11 +1,7 @@
-"""Synthetic conversation workloads and the sharded dataset simulation.
+"""The c5 synthetic conversation workload (simulated by simulate.py and bench.py).
 
 Config c5 (BASELINE.json): 1024 synthetic conversations with an MT-Bench /
-Lmsys-like length distribution, 8B shape, sharded one stream per GPU. The
-reference simulates a dataset with a sequential loop over conversations that
-share one backend (`/root/reference/pkg/src/specstream/metrics.py:202-216`);
-conversations are independent units, so ranks take disjoint
-shards with no per-pass collective and one final gather of metrics.
+Lmsys-like length distribution, 8B shape, one stream per GPU.
 
 Prompt words ~ lognormal(ln 25, 0.6) clipped to [4, 120]; half of the
 conversations have a second turn; words are uniform over the non-special ids
@@ -19,11 +15,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from ._specstream import specstream
-from .fused import run_conversation
 
 PipelineConfig = specstream.PipelineConfig
 Conversation = specstream.Conversation
-compute_metrics = specstream.compute_metrics
 
 
 @dataclass(frozen=True)
@@ -70,18 +64,3 @@ def c5_config(vocab, spec: WorkloadSpec = WorkloadSpec(), **overrides) -> Pipeli
                 rate_chars_per_min=600.0)
     base.update(overrides)
     return PipelineConfig(**base)
-
-
-def shard(items, rank: int, world: int):
-    """Static round-robin shard (conversation i -> rank i mod world)."""
-    return items[rank::world]
-
-
-def simulate(conversations, cfg: PipelineConfig, lm, baseline: bool = False):
-    """Run conversations in order on one backend; (metrics records, turn results)."""
-    records, results = [], []
-    for conv in conversations:
-        for res in run_conversation(conv.turns, cfg, lm, conversation_id=conv.id, baseline=baseline):
-            records.append(compute_metrics(res.events))
-            results.append(res)
-    return records, results
