@@ -227,7 +227,34 @@ def make_tiny_topk(n_turns: int = 5):
     print("topk turns kept:", len(turns), "of", trial)
 
 
+def make_tiny_generator(generator: str = "jacobi", n_turns: int = 4):
+    """Config c1 with the reference's Jacobi generator (generate.py:181-291) on the float64
+    oracle decoder: full event logs, kept when every consumed row's top-2 gap > GAP_MIN."""
+    shape = TINY.as_dict()
+    vocab = SyntheticVocabulary(TINY.vocab)
+    cfg = RefConfig(system_prompt="", chunk_words=8, max_response_tokens=32, generator=generator)
+    turns, trial = [], 0
+    while len(turns) < n_turns and trial < 30:
+        rng = np.random.default_rng(7900 + trial)
+        text = tiny_prompt(rng, vocab, 64)
+        lm = CpuDecoderLM(shape, vocab, seed=0, latency=ref_lm.LatencyModel())
+        res = ref.run_turn([], ref.make_stream(text, cfg.rate_chars_per_min, cfg.chunk_words), cfg, lm)
+        rec = {"trial": trial, "prompt": text, "speculative": {"final_text": res.final_text, "nfe_total": res.nfe_total,
+                                                              "events": events_json(res), "min_gap": float(lm.min_gap)}}
+        kinds = sorted({e["pass_kind"] for e in rec["speculative"]["events"] if e["kind"] == "generate_step"})
+        print(generator, "trial", trial, "passes", kinds, "gap", lm.min_gap, flush=True)
+        if lm.min_gap > GAP_MIN:
+            turns.append(rec)
+        trial += 1
+    (HERE / f"tiny_{generator}_turns.json").write_text(json.dumps({"shape": shape, "config": f"c1-{generator}",
+                                                                  "seed": 0, "turns": turns}, sort_keys=True) + "\n")
+    print(generator, "turns kept:", len(turns), "of", trial)
+
+
 if __name__ == "__main__":
+    if "--jacobi" in sys.argv:
+        make_tiny_generator("jacobi")
+        sys.exit(0)
     if "--c2" in sys.argv:
         make_c2()
         sys.exit(0)

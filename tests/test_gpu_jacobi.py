@@ -11,7 +11,7 @@ does not depend on how many rows the pass scored).
 import numpy as np
 import pytest
 
-from conftest import GOLDEN  # noqa: F401
+from conftest import GOLDEN
 from paper_2506_15556_b200 import B200LM, greedy_decode, jacobi_generate, specstream
 from paper_2506_15556_b200.shapes import TINY, small_shape
 
@@ -33,5 +33,26 @@ def test_jacobi_fixed_point_equals_greedy(shape):
             want = greedy_decode(lm, p + r[:k], max_new=window)[len(p) + k:]
             assert out.response[k:] == want
             assert sum(1 for x in out.passes if x.kind == "jacobi") <= max(1, window)
+    finally:
+        lm.close()
+
+
+JACOBI_TURNS = __import__("json").loads((GOLDEN / "tiny_jacobi_turns.json").read_text())
+
+
+@pytest.mark.parametrize("i", range(len(JACOBI_TURNS["turns"])))
+def test_jacobi_turns_equal_reference_golden(i):
+    """Whole c1 turns with the reference's Jacobi generator (generate.py:181-291) on
+    B200LM reproduce the event logs the reference produced on the float64 oracle
+    decoder (tests/golden/tiny_jacobi_turns.json): every jacobi / prefill / decode
+    pass, every verify k, every timestamp."""
+    rec = JACOBI_TURNS["turns"][i]
+    cfg = specstream.PipelineConfig(system_prompt="", chunk_words=8, max_response_tokens=32, generator="jacobi")
+    lm = B200LM(TINY, seed=JACOBI_TURNS["seed"], max_seq=1024)
+    try:
+        res = specstream.run_turn([], specstream.make_stream(rec["prompt"], cfg.rate_chars_per_min, cfg.chunk_words),
+                                  cfg, lm)
+        assert res.final_text == rec["speculative"]["final_text"]
+        assert [e.to_dict() for e in res.events] == rec["speculative"]["events"]
     finally:
         lm.close()
