@@ -68,6 +68,27 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// warp_sum of V values at once, transposed: at each xor level a lane keeps
+// half of its values and trades the other half with its partner, so the V
+// sums cost V - 2 shuffles instead of 5V. Every sum is formed by exactly
+// warp_sum's adds (own + partner at offsets 16, 8, 4, 2, 1), hence bitwise
+// equal to it. On return lane l holds the sums of values V/32*l .. +V/32-1
+// in a[0 .. V/32-1].
+template <int V>
+__device__ __forceinline__ void warp_sum_transposed(float (&a)[V], int lane) {
+  static_assert(V % 32 == 0, "V must be a multiple of 32");
+#pragma unroll
+  for (int o = 16, m = V; o > 0; o >>= 1, m >>= 1) {
+    const bool hi = lane & o;  // keeps the upper half
+#pragma unroll
+    for (int j = 0; j < m / 2; ++j) {
+      const float keep = hi ? a[j + m / 2] : a[j];
+      const float send = hi ? a[j] : a[j + m / 2];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
 __device__ __forceinline__ int warp_sum_int(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -67,20 +67,103 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict
   }
 }
 
+// Lane-slice partials of R weight rows x TT staged tokens over one K-split:
+// lane l accumulates the float4 chunks c ≡ l (mod 32) in order (the decode
+// GEMV's order), with the next chunk's weights in flight.
+template <int TT, int R>
+__device__ __forceinline__ void rows_x_tokens(float (&a)[R * TT], const float4* const (&w)[R], const float4* xs4,
+                                              int nvec, int lane) {
+#pragma unroll
+  for (int v = 0; v < R * TT; ++v) a[v] = 0.f;
+  float4 wc[R];
+  if (lane < nvec) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) wc[i] = __ldg(w[i] + lane);
+  }
+  for (int c = lane; c < nvec; c += 32) {
+    float4 wn[R];
+    if (c + 32 < nvec) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) wn[i] = __ldg(w[i] + c + 32);
+    }
+#pragma unroll
+    for (int t = 0; t < TT; ++t) {
+      const float4 x = xs4[t * nvec + c];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        float& d = a[i * TT + t];
+        d = fmaf(x.x, wc[i].x, d); d = fmaf(x.y, wc[i].y, d);
+        d = fmaf(x.z, wc[i].z, d); d = fmaf(x.w, wc[i].w, d);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) wc[i] = wn[i];
+  }
+}
+
+// Wide passes: a warp owns R output rows x TT tokens (R*TT = 64 lane-slice
+// partials per lane), so each staged x float4 feeds 4R FMAs and each weight
+// float4 4*TT; the next chunk's weights are in flight while the current one
+// is consumed. Lane l still accumulates exactly the chunks c ≡ l (mod 32) of
+// the K-split in order, and the 32 lane partials of every output are summed
+// by a transposed butterfly whose adds are warp_sum's (same pairs, same
+// order), so every output is bitwise the decode GEMV's.
+template <int TT, int R>
+__global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __restrict__ ctx,
+                                                               const float* __restrict__ X, int ldx,
+                                                               const float* __restrict__ W, float* __restrict__ part,
+                                                               int N, int K, int ksplit) {
+  static_assert(R * TT == 64, "the transposed butterfly leaves 2 of the 64 sums per lane");
+  pdl_enter();
+  extern __shared__ float4 xs4[];
+  if (ctx->stop) return;
+  const int rows = ctx->rows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = blockIdx.x * (8 * R) + warp * R;
+  const int s = blockIdx.y;
+  const int kbeg = s * ksplit;
+  const int nvec = ksplit >> 2;
+  const float4* w[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) w[i] = reinterpret_cast<const float4*>(W + size_t(min(nb + i, N - 1)) * K + kbeg);
+  for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
+    const int nt = min(TT, rows - tt);
+    __syncthreads();
+    for (int e = threadIdx.x; e < TT * nvec; e += 256) {
+      const int t = e / nvec, c = e % nvec;
+      xs4[e] = t < nt ? reinterpret_cast<const float4*>(X + size_t(tt + t) * ldx + kbeg)[c]
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    float a[R * TT];
+    rows_x_tokens<TT, R>(a, w, xs4, nvec, lane);
+    warp_sum_transposed<R * TT>(a, lane);
+    // lane l now holds the sums of values 2l and 2l + 1 (value = i * TT + t)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int v = 2 * lane + j, i = v / TT, t = v % TT;
+      if (t < nt && nb + i < N) part[(size_t(s) * kMaxWindow + tt + t) * N + nb + i] = a[j];
+    }
+  }
+}
+
 void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, const float* W,
                      float* part, int N, int K, int splits, cudaStream_t st) {
   const int ksplit = K / splits;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_f32_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_f32_wide_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(gemm_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(N / 16, splits, max_rows <= 1 ? 1 : (max_rows + 15) / 16);
-  if (max_rows <= 1)
-    launch_pdl(gemm_f32_kernel<1>, dim3(grid), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part, N, K, ksplit);
-  else
-    launch_pdl(gemm_f32_kernel<16>, dim3(grid), dim3(256), size_t(ksplit) * 16 * 4, st, ctx, X, ldx, W, part, N, K, ksplit);
+  if (max_rows <= 1) {
+    launch_pdl(gemm_f32_kernel<1>, dim3(N / 16, splits, 1), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part,
+               N, K, ksplit);
+  } else {
+    const dim3 grid((N + 31) / 32, splits, (max_rows + 15) / 16);
+    launch_pdl(gemm_f32_wide_kernel<16, 4>, grid, dim3(256), size_t(ksplit) * 16 * 4, st, ctx, X, ldx, W, part, N, K,
+               ksplit);
+  }
 }
 
 // LM head: 64 vocab ids per CTA (8 warps x 2 rows x 4 passes), fused
@@ -163,13 +246,94 @@ __global__ void __launch_bounds__(256) lmhead_f32_kernel(PassCtx* ctx, const flo
   }
 }
 
+// Wide passes: 64 vocab ids per CTA as 2 passes of 8 warps x 4 rows, each
+// warp's 4 rows x 16 tokens summed with the transposed butterfly (bitwise the
+// decode kernel's warp_sum), then bias and the (max, lowest id) merge.
+template <int TT, int R>
+__global__ void __launch_bounds__(256, 2) lmhead_f32_wide_kernel(PassCtx* ctx, const float* __restrict__ hn_cache,
+                                                                 const float* __restrict__ W,
+                                                                 const float* __restrict__ bias, int v_begin,
+                                                                 int v_count, int H, float* __restrict__ am_val,
+                                                                 int* __restrict__ am_idx,
+                                                                 float* __restrict__ logits_out, int ld_logits) {
+  static_assert(R * TT == 64 && TT == 16, "lane l ends with tokens 2(l & 7), +1 of row l >> 3");
+  pdl_enter();
+  extern __shared__ float4 xs4[];
+  __shared__ float bv[8][TT];
+  __shared__ int bi[8][TT];
+  if (ctx->stop) return;
+  const int rows = ctx->rows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = H >> 2;
+  const int ntiles = (v_count + kLmTileF32 - 1) / kLmTileF32;
+  const int Z = int(gridDim.x) / ntiles, tile = blockIdx.x / Z, z = blockIdx.x % Z;
+  const float* X = hn_cache + size_t(ctx->n0) * H;
+  const int i_mine = lane >> 3, t_mine = 2 * (lane & 7);
+  for (int tt = z * TT; tt < rows; tt += TT * Z) {
+    const int nt = min(TT, rows - tt);
+    __syncthreads();
+    for (int e = threadIdx.x; e < TT * nvec; e += 256) {
+      const int t = e / nvec, c = e % nvec;
+      xs4[e] = t < nt ? reinterpret_cast<const float4*>(X + size_t(tt + t) * H)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    float best[2] = {-INFINITY, -INFINITY};
+    int besti[2] = {0x7fffffff, 0x7fffffff};
+    for (int it = 0; it < kLmTileF32 / (8 * R); ++it) {
+      const int r0 = tile * kLmTileF32 + it * 8 * R + warp * R;  // local vocab row
+      if (r0 >= v_count) break;
+      const float4* w[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) w[i] = reinterpret_cast<const float4*>(W + size_t(min(r0 + i, v_count - 1)) * H);
+      float a[R * TT];
+      rows_x_tokens<TT, R>(a, w, xs4, nvec, lane);
+      warp_sum_transposed<R * TT>(a, lane);
+      const int r = r0 + i_mine;
+      if (r < v_count) {
+        const float b = bias[v_begin + r];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int t = t_mine + j;
+          const float l = a[j] + b;
+          if (t < nt) {
+            argmax_merge(best[j], besti[j], l, v_begin + r);
+            if (logits_out) logits_out[size_t(tt + t) * ld_logits + r] = l;
+          }
+        }
+      }
+    }
+    // the 4 lanes holding the same tokens (lane & 7 equal) merge; lanes 0-7 publish
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, best[j], o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, besti[j], o);
+        argmax_merge(best[j], besti[j], v2, i2);
+      }
+      if (lane < 8) {
+        bv[warp][t_mine + j] = best[j];
+        bi[warp][t_mine + j] = besti[j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nt) {
+      float v = bv[0][threadIdx.x];
+      int i = bi[0][threadIdx.x];
+      for (int w = 1; w < 8; ++w) argmax_merge(v, i, bv[w][threadIdx.x], bi[w][threadIdx.x]);
+      am_val[size_t(tile) * kMaxWindow + tt + threadIdx.x] = v;
+      am_idx[size_t(tile) * kMaxWindow + tt + threadIdx.x] = i;
+    }
+  }
+}
+
 void launch_lmhead_f32(const PassCtx* ctx, int max_rows, const float* hn_cache, int pos_offset,
                        const float* W, const float* bias, int v_begin, int v_count, int hidden,
                        float* am_val, int* am_idx, float* logits_out, int ld_logits, cudaStream_t st) {
   (void)pos_offset;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lmhead_f32_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lmhead_f32_wide_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(lmhead_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
@@ -180,7 +344,7 @@ void launch_lmhead_f32(const PassCtx* ctx, int max_rows, const float* hn_cache, 
                                                                  am_val, am_idx, logits_out, ld_logits);
   else {
     const int Z = (max_rows + 15) / 16;  // token chunks per vocab tile (gridDim.x = tiles * Z)
-    launch_pdl(lmhead_f32_kernel<16>, dim3(tiles * Z), dim3(256), size_t(hidden) * 16 * 4, st, 
+    launch_pdl(lmhead_f32_wide_kernel<16, 4>, dim3(tiles * Z), dim3(256), size_t(hidden) * 16 * 4, st, 
         c, hn_cache, W, bias, v_begin, v_count, hidden, am_val, am_idx, logits_out, ld_logits);
   }
 }

@@ -141,6 +141,21 @@ def test_batch_invariance_bitwise_whole_tiles(n):
         lm.close()
 
 
+def test_batch_invariance_bitwise_f32_c2_shape():
+    """fp32 at the c2 (Qwen2.5-0.5B) shape: the wide GEMM (4 rows x 16 tokens per
+    warp, transposed butterfly) and the decode GEMV give bitwise the same rows,
+    including the down projection's uneven lane chunk counts (K-split 608 floats)."""
+    from paper_2506_15556_b200.shapes import QWEN_05B
+
+    lm = B200LM(QWEN_05B, seed=0, max_seq=512)
+    try:
+        toks = rand_tokens(np.random.default_rng(7), lm.vocab_size, 40)
+        one, step = _rows_one_pass_vs_stepwise(lm, toks)
+        assert np.array_equal(one.view(np.uint32), step.view(np.uint32))
+    finally:
+        lm.close()
+
+
 def test_batch_invariance_and_agreement_hd64():
     """head_dim 64 on the bf16 path (two heads per 128-row QKV tile, 64-dim RoPE
     rows, half-warp attention merges): bitwise batch invariance and agreement with
