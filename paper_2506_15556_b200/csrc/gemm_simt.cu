@@ -11,14 +11,42 @@
 
 namespace ps {
 
-template <int TT>
-__global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict__ ctx, const float* __restrict__ X,
-                                                       int ldx, const float* __restrict__ W, float* __restrict__ part,
-                                                       int N, int K, int ksplit) {
-  pdl_enter();
+// L2 prefetch of `nrows` weight rows (`floats` each, `ld` apart) by one warp,
+// one request per 128-byte line. Issued BEFORE the programmatic-dependency
+// wait: weights never depend on the previous kernel of the chain, so their
+// DRAM latency overlaps its tail. (Register loads cannot be placed there —
+// ptxas hoists griddepcontrol.wait above every LDG — but prefetches and
+// cp.async stay where they are written.)
+__device__ __forceinline__ void prefetch_rows_l2(const float* base, size_t ld, int nrows, int floats, int lane) {
+  for (int r = 0; r < nrows; ++r)
+    for (int off = lane * 32; off < floats; off += 32 * 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + r * ld + off));
+}
+
+// x rows [tt, tt + TT) of this K-split -> shared memory, every 16-byte copy in
+// flight at once (cp.async; rows past nt are zero-filled). One round trip
+// instead of one per loop iteration.
+__device__ __forceinline__ void stage_x_async(float4* xs4, const float* X, size_t ldx, int kbeg, int tt, int nt, int TT,
+                                              int nvec) {
+  for (int e = threadIdx.x; e < TT * nvec; e += blockDim.x) {
+    const int t = e / nvec, c = e % nvec;
+    const float* src = X + size_t(tt + min(t, nt - 1)) * ldx + kbeg + 4 * c;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(xs4 + e));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(t < nt ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// Decode GEMV (1 row). The warp's two weight rows are prefetched into L2
+// before the programmatic-dependency wait; after it, each lane requests all of
+// its chunks (up to kPre per row) at once, together with the staged x. The
+// FMA order (chunks c = lane, lane + 32, ... ascending, then warp_sum) is the
+// wide kernels' (batch invariance).
+constexpr int kGemvPre = 8;
+__global__ void __launch_bounds__(256) gemm_f32_gemv_kernel(const PassCtx* __restrict__ ctx, const float* __restrict__ X,
+                                                            int ldx, const float* __restrict__ W,
+                                                            float* __restrict__ part, int N, int K, int ksplit) {
   extern __shared__ float4 xs4[];
-  if (ctx->stop) return;
-  const int rows = ctx->rows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * 16 + warp * 2;
   const int s = blockIdx.y;
@@ -26,44 +54,45 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict
   const int nvec = ksplit >> 2;
   const float4* w0 = reinterpret_cast<const float4*>(W + size_t(n0) * K + kbeg);
   const float4* w1 = reinterpret_cast<const float4*>(W + size_t(n0 + 1) * K + kbeg);
-  // blockIdx.z takes every gridDim.z-th chunk of TT tokens (more CTAs for
-  // narrow N; the per-output arithmetic does not depend on the chunking)
-  for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
-    const int nt = min(TT, rows - tt);
-    __syncthreads();
-    for (int e = threadIdx.x; e < TT * nvec; e += 256) {
-      const int t = e / nvec, c = e % nvec;
-      xs4[e] = t < nt ? reinterpret_cast<const float4*>(X + size_t(tt + t) * ldx + kbeg)[c]
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __syncthreads();
-    float a0[TT], a1[TT];
+  prefetch_rows_l2(W + size_t(n0) * K + kbeg, K, 2, ksplit, lane);
+  pdl_enter();
+  if (ctx->stop || ctx->rows < 1) return;
+  float4 u[kGemvPre], v[kGemvPre];
 #pragma unroll
-    for (int t = 0; t < TT; ++t) a0[t] = a1[t] = 0.f;
-    for (int c = lane; c < nvec; c += 32) {
-      const float4 u = __ldg(w0 + c), v = __ldg(w1 + c);
-#pragma unroll
-      for (int t = 0; t < TT; ++t) {
-        const float4 x = xs4[t * nvec + c];
-        a0[t] = fmaf(x.x, u.x, a0[t]); a0[t] = fmaf(x.y, u.y, a0[t]);
-        a0[t] = fmaf(x.z, u.z, a0[t]); a0[t] = fmaf(x.w, u.w, a0[t]);
-        a1[t] = fmaf(x.x, v.x, a1[t]); a1[t] = fmaf(x.y, v.y, a1[t]);
-        a1[t] = fmaf(x.z, v.z, a1[t]); a1[t] = fmaf(x.w, v.w, a1[t]);
-      }
+  for (int i = 0; i < kGemvPre; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nvec) {
+      u[i] = __ldg(w0 + c);
+      v[i] = __ldg(w1 + c);
     }
+  }
+  for (int e = threadIdx.x; e < nvec; e += 256) xs4[e] = reinterpret_cast<const float4*>(X + kbeg)[e];
+  __syncthreads();
+  float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-    for (int t = 0; t < TT; ++t) {
-      a0[t] = warp_sum(a0[t]);
-      a1[t] = warp_sum(a1[t]);
+  for (int i = 0; i < kGemvPre; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nvec) {
+      const float4 x = xs4[c];
+      a0 = fmaf(x.x, u[i].x, a0); a0 = fmaf(x.y, u[i].y, a0);
+      a0 = fmaf(x.z, u[i].z, a0); a0 = fmaf(x.w, u[i].w, a0);
+      a1 = fmaf(x.x, v[i].x, a1); a1 = fmaf(x.y, v[i].y, a1);
+      a1 = fmaf(x.z, v[i].z, a1); a1 = fmaf(x.w, v[i].w, a1);
     }
-#pragma unroll
-    for (int t = 0; t < TT; ++t) {
-      if (lane == t && t < nt) {
-        float* o = part + (size_t(s) * kMaxWindow + tt + t) * N + n0;
-        o[0] = a0[t];
-        o[1] = a1[t];
-      }
-    }
+  }
+  for (int c = lane + 32 * kGemvPre; c < nvec; c += 32) {  // K-splits longer than 32 * kPre chunks
+    const float4 uu = __ldg(w0 + c), vv = __ldg(w1 + c), x = xs4[c];
+    a0 = fmaf(x.x, uu.x, a0); a0 = fmaf(x.y, uu.y, a0);
+    a0 = fmaf(x.z, uu.z, a0); a0 = fmaf(x.w, uu.w, a0);
+    a1 = fmaf(x.x, vv.x, a1); a1 = fmaf(x.y, vv.y, a1);
+    a1 = fmaf(x.z, vv.z, a1); a1 = fmaf(x.w, vv.w, a1);
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  if (lane == 0) {
+    float* o = part + size_t(s) * kMaxWindow * N + n0;
+    o[0] = a0;
+    o[1] = a1;
   }
 }
 
@@ -72,14 +101,12 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const PassCtx* __restrict
 // GEMV's order), with the next chunk's weights in flight.
 template <int TT, int R>
 __device__ __forceinline__ void rows_x_tokens(float (&a)[R * TT], const float4* const (&w)[R], const float4* xs4,
-                                              int nvec, int lane) {
+                                              int nvec, int lane, const float4 (&w_first)[R]) {
 #pragma unroll
   for (int v = 0; v < R * TT; ++v) a[v] = 0.f;
   float4 wc[R];
-  if (lane < nvec) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) wc[i] = __ldg(w[i] + lane);
-  }
+  for (int i = 0; i < R; ++i) wc[i] = w_first[i];
   for (int c = lane; c < nvec; c += 32) {
     float4 wn[R];
     if (c + 32 < nvec) {
@@ -114,10 +141,7 @@ __global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __
                                                                const float* __restrict__ W, float* __restrict__ part,
                                                                int N, int K, int ksplit) {
   static_assert(R * TT == 64, "the transposed butterfly leaves 2 of the 64 sums per lane");
-  pdl_enter();
   extern __shared__ float4 xs4[];
-  if (ctx->stop) return;
-  const int rows = ctx->rows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = blockIdx.x * (8 * R) + warp * R;
   const int s = blockIdx.y;
@@ -126,17 +150,24 @@ __global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __
   const float4* w[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) w[i] = reinterpret_cast<const float4*>(W + size_t(min(nb + i, N - 1)) * K + kbeg);
+  // the warp's weight rows do not depend on the previous kernel: into L2
+  // before the programmatic-dependency wait
+  prefetch_rows_l2(W + size_t(min(nb, N - 1)) * K + kbeg, K, min(R, N - nb), ksplit, lane);
+  pdl_enter();
+  if (ctx->stop) return;
+  float4 wf[R];
+  if (lane < nvec) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) wf[i] = __ldg(w[i] + lane);
+  }
+  const int rows = ctx->rows;
   for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
     const int nt = min(TT, rows - tt);
     __syncthreads();
-    for (int e = threadIdx.x; e < TT * nvec; e += 256) {
-      const int t = e / nvec, c = e % nvec;
-      xs4[e] = t < nt ? reinterpret_cast<const float4*>(X + size_t(tt + t) * ldx + kbeg)[c]
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    stage_x_async(xs4, X, ldx, kbeg, tt, nt, TT, nvec);
     __syncthreads();
     float a[R * TT];
-    rows_x_tokens<TT, R>(a, w, xs4, nvec, lane);
+    rows_x_tokens<TT, R>(a, w, xs4, nvec, lane, wf);
     warp_sum_transposed<R * TT>(a, lane);
     // lane l now holds the sums of values 2l and 2l + 1 (value = i * TT + t)
 #pragma unroll
@@ -153,11 +184,11 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_f32_wide_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(gemm_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_f32_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (max_rows <= 1) {
-    launch_pdl(gemm_f32_kernel<1>, dim3(N / 16, splits, 1), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part,
+    launch_pdl(gemm_f32_gemv_kernel, dim3(N / 16, splits, 1), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part,
                N, K, ksplit);
   } else {
     const dim3 grid((N + 31) / 32, splits, (max_rows + 15) / 16);
@@ -257,25 +288,22 @@ __global__ void __launch_bounds__(256, 2) lmhead_f32_wide_kernel(PassCtx* ctx, c
                                                                  int* __restrict__ am_idx,
                                                                  float* __restrict__ logits_out, int ld_logits) {
   static_assert(R * TT == 64 && TT == 16, "lane l ends with tokens 2(l & 7), +1 of row l >> 3");
-  pdl_enter();
   extern __shared__ float4 xs4[];
   __shared__ float bv[8][TT];
   __shared__ int bi[8][TT];
-  if (ctx->stop) return;
-  const int rows = ctx->rows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = H >> 2;
   const int ntiles = (v_count + kLmTileF32 - 1) / kLmTileF32;
   const int Z = int(gridDim.x) / ntiles, tile = blockIdx.x / Z, z = blockIdx.x % Z;
+  pdl_enter();
+  if (ctx->stop) return;
+  const int rows = ctx->rows;
   const float* X = hn_cache + size_t(ctx->n0) * H;
   const int i_mine = lane >> 3, t_mine = 2 * (lane & 7);
   for (int tt = z * TT; tt < rows; tt += TT * Z) {
     const int nt = min(TT, rows - tt);
     __syncthreads();
-    for (int e = threadIdx.x; e < TT * nvec; e += 256) {
-      const int t = e / nvec, c = e % nvec;
-      xs4[e] = t < nt ? reinterpret_cast<const float4*>(X + size_t(tt + t) * H)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    stage_x_async(xs4, X, H, 0, tt, nt, TT, nvec);
     __syncthreads();
     float best[2] = {-INFINITY, -INFINITY};
     int besti[2] = {0x7fffffff, 0x7fffffff};
@@ -285,8 +313,13 @@ __global__ void __launch_bounds__(256, 2) lmhead_f32_wide_kernel(PassCtx* ctx, c
       const float4* w[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) w[i] = reinterpret_cast<const float4*>(W + size_t(min(r0 + i, v_count - 1)) * H);
+      float4 wf[R];
+      if (lane < nvec) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) wf[i] = __ldg(w[i] + lane);
+      }
       float a[R * TT];
-      rows_x_tokens<TT, R>(a, w, xs4, nvec, lane);
+      rows_x_tokens<TT, R>(a, w, xs4, nvec, lane, wf);
       warp_sum_transposed<R * TT>(a, lane);
       const int r = r0 + i_mine;
       if (r < v_count) {

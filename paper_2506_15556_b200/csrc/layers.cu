@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __rest
   const int pos = ctx->n0 + t;
   const int hd = g.head_dim, half = hd >> 1;
   const int nq = heads * half, nk = g.kv_heads * half;
+  // one (pair) item per thread: blockIdx.y spreads the row's items over CTAs,
+  // so a 1-row decode pass has all its loads in flight at once
   const size_t sstride = size_t(kMaxWindow) * N;
   const float* pr = part + size_t(t) * N;
   auto sum_col = [&](int c) {
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(128) qkv_finalize_kernel(const PassCtx* __rest
   const size_t page = size_t(page_table[pos / kPage]);
   const int slot = pos % kPage;
   const size_t lbase = size_t(layer) * g.layer_stride();
-  for (int p = threadIdx.x; p < nq + 2 * nk; p += blockDim.x) {
+  for (int p = blockIdx.y * blockDim.x + threadIdx.x; p < nq + 2 * nk; p += blockDim.x * gridDim.y) {
     if (p < nq + nk) {
       const bool is_q = p < nq;
       const int pp = is_q ? p : p - nq;
@@ -125,8 +127,9 @@ template <typename T>
 void launch_qkv_finalize(const PassCtx* ctx, int max_rows, const float* part, int splits, int ldp,
                          const T* bias, const float2* rope, T* q, T* kpool, T* vpool,
                          const int* page_table, KvGeom g, int layer, int heads, cudaStream_t st) {
-  launch_pdl(qkv_finalize_kernel<T>, dim3(max_rows), dim3(128), 0, st, ctx, part, splits, ldp, bias, rope, q, kpool, vpool,
-                                                   page_table, g, layer, heads);
+  const int items = (heads + 2 * g.kv_heads) * g.head_dim / 2;
+  launch_pdl(qkv_finalize_kernel<T>, dim3(max_rows, (items + 127) / 128), dim3(128), 0, st, ctx, part, splits, ldp, bias,
+             rope, q, kpool, vpool, page_table, g, layer, heads);
 }
 
 // ---------------------------------------------------------------------------
@@ -242,11 +245,28 @@ __global__ void __launch_bounds__(256) residual_norm_kernel(const PassCtx* __res
   float* xr = x + size_t(t) * H;
   const float* pr = part + size_t(t) * H;
   float ss = 0.f;
-  for (int c = threadIdx.x; c < H; c += 256) {
-    const float d = f32_sum_splits(pr + c, splits, sstride);
-    const float v = __fadd_rn(xr[c], d);
-    xr[c] = v;
-    ss = fmaf(v, v, ss);
+  // elements c = tid, tid + 256, ... in order; kBatch of them with every load
+  // (residual and split partials) in flight before the first add
+  constexpr int kBatch = 4;
+  for (int c0 = threadIdx.x; c0 < H; c0 += 256 * kBatch) {
+    float xv[kBatch], dv[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int c = c0 + 256 * j;
+      if (c < H) {
+        xv[j] = xr[c];
+        dv[j] = f32_sum_splits(pr + c, splits, sstride);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int c = c0 + 256 * j;
+      if (c < H) {
+        const float v = __fadd_rn(xv[j], dv[j]);
+        xr[c] = v;
+        ss = fmaf(v, v, ss);
+      }
+    }
   }
   ss = block_sum<256>(ss, red);
   const float rstd = f32_rstd(ss, H, eps);
