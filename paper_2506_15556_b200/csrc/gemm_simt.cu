@@ -129,53 +129,144 @@ __device__ __forceinline__ void rows_x_tokens(float (&a)[R * TT], const float4* 
 }
 
 // Wide passes: a warp owns R output rows x TT tokens (R*TT = 64 lane-slice
-// partials per lane), so each staged x float4 feeds 4R FMAs and each weight
-// float4 4*TT; the next chunk's weights are in flight while the current one
-// is consumed. Lane l still accumulates exactly the chunks c ≡ l (mod 32) of
-// the K-split in order, and the 32 lane partials of every output are summed
-// by a transposed butterfly whose adds are warp_sum's (same pairs, same
-// order), so every output is bitwise the decode GEMV's.
+// partials per lane), so each staged x float4 feeds 4R FMAs. Lane l still
+// accumulates exactly the chunks c ≡ l (mod 32) of the K-split in order, and
+// the 32 lane partials of every output are summed by a transposed butterfly
+// whose adds are warp_sum's (same pairs, same order), so every output is
+// bitwise the decode GEMV's.
+// A CTA stages its TT-token chunk of x once and then walks its units j =
+// blockIdx.x, + gridDim.x, ...; a unit is U consecutive 8R-row sub-tiles.
+// Weight chunks stream through a per-warp 3-stage shared-memory ring with
+// cp.async, two chunks ahead and across sub-tile boundaries: each lane copies
+// and later reads only its own chunks, so a per-thread wait_group is the only
+// synchronisation. (Register prefetch of the next chunk was sunk by the
+// compiler to the end of the current one, and every chunk then waited a full
+// L2/DRAM round trip.) epi(sums, first row of the warp, tt, nt) gets the two
+// sums lane l holds after the butterfly (values 2l, 2l + 1; value = i*TT + t);
+// unit_done(j) runs after each unit.
+constexpr int kWideStages = 3;
+template <int TT, int R, int U, class Epi, class UnitDone>
+__device__ __forceinline__ void wide_walk(const float* __restrict__ W, int N, int K, int kbeg, int nvec, int units,
+                                          const float* __restrict__ X, int ldx, int rows, float4* xs4, Epi&& epi,
+                                          UnitDone&& unit_done) {
+  static_assert(R * TT == 64, "the transposed butterfly leaves 2 of the 64 sums per lane");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kmax = (nvec + 31) / 32;  // chunk steps per sub-tile (lanes past nvec%32 skip the last)
+  const int my_units = int(blockIdx.x) < units ? (units - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  const int total = my_units * U * kmax;
+  float4* ring = xs4 + TT * nvec + warp * (kWideStages * R * 32);  // [stage][R][lane]
+  auto first_row = [&](int q) {  // first weight row of this warp in chunk step q's sub-tile
+    const int st = q / kmax;
+    return ((int(blockIdx.x) + (st / U) * int(gridDim.x)) * U + st % U) * (8 * R) + warp * R;
+  };
+  auto issue = [&](int q) {
+    if (q < total) {
+      const int c = lane + 32 * (q % kmax);
+      if (c < nvec) {
+        const int nb = first_row(q);
+        float4* dst = ring + (q % kWideStages) * (R * 32) + lane;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + i * 32));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                       "l"(W + size_t(min(nb + i, N - 1)) * K + kbeg + 4 * c)
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
+    const int nt = min(TT, rows - tt);
+    __syncthreads();
+    issue(0);
+    issue(1);
+    stage_x_async(xs4, X, ldx, kbeg, tt, nt, TT, nvec);  // (waits for every group: chunks 0, 1 too)
+    __syncthreads();
+    int q = 0;
+    for (int j = blockIdx.x; j < units; j += gridDim.x) {
+      for (int u = 0; u < U; ++u) {
+        const int nb = first_row(q);
+        float a[R * TT];
+#pragma unroll
+        for (int v = 0; v < R * TT; ++v) a[v] = 0.f;
+        for (int k = 0; k < kmax; ++k, ++q) {
+          issue(q + 2);
+          asm volatile("cp.async.wait_group 2;" ::: "memory");
+          const int c = lane + 32 * k;
+          if (c < nvec) {
+            const float4* wr = ring + (q % kWideStages) * (R * 32) + lane;
+            float4 wc[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i) wc[i] = wr[i * 32];
+#pragma unroll
+            for (int t = 0; t < TT; ++t) {
+              const float4 x = xs4[t * nvec + c];
+#pragma unroll
+              for (int i = 0; i < R; ++i) {
+                float& d = a[i * TT + t];
+                d = fmaf(x.x, wc[i].x, d); d = fmaf(x.y, wc[i].y, d);
+                d = fmaf(x.z, wc[i].z, d); d = fmaf(x.w, wc[i].w, d);
+              }
+            }
+          }
+        }
+        warp_sum_transposed<R * TT>(a, lane);
+        epi(a, nb, tt, nt);
+      }
+      unit_done(j, tt, nt);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // no copy into the ring outlives this chunk of x
+  }
+}
+
+// this warp's weight rows of every unit the CTA will walk do not depend on the
+// previous kernel: into L2 before the programmatic-dependency wait
+template <int R, int U>
+__device__ __forceinline__ void wide_prefetch(const float* W, int N, int K, int kbeg, int ksplit, int units) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x; j < units; j += gridDim.x)
+    for (int u = 0; u < U; ++u) {
+      const int nb = (j * U + u) * (8 * R) + warp * R;
+      if (nb < N) prefetch_rows_l2(W + size_t(nb) * K + kbeg, K, min(R, N - nb), ksplit, lane);
+    }
+}
+
 template <int TT, int R>
 __global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __restrict__ ctx,
                                                                const float* __restrict__ X, int ldx,
                                                                const float* __restrict__ W, float* __restrict__ part,
                                                                int N, int K, int ksplit) {
-  static_assert(R * TT == 64, "the transposed butterfly leaves 2 of the 64 sums per lane");
   extern __shared__ float4 xs4[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = blockIdx.x * (8 * R) + warp * R;
-  const int s = blockIdx.y;
-  const int kbeg = s * ksplit;
-  const int nvec = ksplit >> 2;
-  const float4* w[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) w[i] = reinterpret_cast<const float4*>(W + size_t(min(nb + i, N - 1)) * K + kbeg);
-  // the warp's weight rows do not depend on the previous kernel: into L2
-  // before the programmatic-dependency wait
-  prefetch_rows_l2(W + size_t(min(nb, N - 1)) * K + kbeg, K, min(R, N - nb), ksplit, lane);
+  const int lane = threadIdx.x & 31;
+  const int ntiles = (N + 8 * R - 1) / (8 * R);
+  const int s = blockIdx.y, kbeg = s * ksplit;
+  wide_prefetch<R, 1>(W, N, K, kbeg, ksplit, ntiles);
   pdl_enter();
   if (ctx->stop) return;
-  float4 wf[R];
-  if (lane < nvec) {
+  wide_walk<TT, R, 1>(
+      W, N, K, kbeg, ksplit >> 2, ntiles, X, ldx, ctx->rows, xs4,
+      [&](const float (&a)[R * TT], int nb, int tt, int nt) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) wf[i] = __ldg(w[i] + lane);
+        for (int jj = 0; jj < 2; ++jj) {
+          const int v = 2 * lane + jj, i = v / TT, t = v % TT;
+          if (t < nt && nb + i < N) part[(size_t(s) * kMaxWindow + tt + t) * N + nb + i] = a[jj];
+        }
+      },
+      [](int, int, int) {});
+}
+
+// CTAs per (K-split, token chunk) of a wide GEMM: about two resident CTAs per
+// SM in total, never more than the tiles
+static int wide_gx(int ntiles, int splits, int z) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
   }
-  const int rows = ctx->rows;
-  for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
-    const int nt = min(TT, rows - tt);
-    __syncthreads();
-    stage_x_async(xs4, X, ldx, kbeg, tt, nt, TT, nvec);
-    __syncthreads();
-    float a[R * TT];
-    rows_x_tokens<TT, R>(a, w, xs4, nvec, lane, wf);
-    warp_sum_transposed<R * TT>(a, lane);
-    // lane l now holds the sums of values 2l and 2l + 1 (value = i * TT + t)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int v = 2 * lane + j, i = v / TT, t = v % TT;
-      if (t < nt && nb + i < N) part[(size_t(s) * kMaxWindow + tt + t) * N + nb + i] = a[j];
-    }
-  }
+  const int per = (ntiles + max(1, 2 * sms / (splits * z)) - 1) / max(1, 2 * sms / (splits * z));  // tiles per CTA
+  return (ntiles + per - 1) / per;
 }
 
 void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, const float* W,
@@ -191,9 +282,10 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
     launch_pdl(gemm_f32_gemv_kernel, dim3(N / 16, splits, 1), dim3(256), size_t(ksplit) * 4, st, ctx, X, ldx, W, part,
                N, K, ksplit);
   } else {
-    const dim3 grid((N + 31) / 32, splits, (max_rows + 15) / 16);
-    launch_pdl(gemm_f32_wide_kernel<16, 4>, grid, dim3(256), size_t(ksplit) * 16 * 4, st, ctx, X, ldx, W, part, N, K,
-               ksplit);
+    const int z = (max_rows + 15) / 16;
+    const dim3 grid(wide_gx((N + 31) / 32, splits, z), splits, z);
+    const size_t smem = size_t(ksplit) * 16 * 4 + size_t(8) * kWideStages * 4 * 32 * 16;  // x chunk + weight rings
+    launch_pdl(gemm_f32_wide_kernel<16, 4>, grid, dim3(256), smem, st, ctx, X, ldx, W, part, N, K, ksplit);
   }
 }
 
@@ -377,8 +469,8 @@ void launch_lmhead_f32(const PassCtx* ctx, int max_rows, const float* hn_cache, 
                                                                  am_val, am_idx, logits_out, ld_logits);
   else {
     const int Z = (max_rows + 15) / 16;  // token chunks per vocab tile (gridDim.x = tiles * Z)
-    launch_pdl(lmhead_f32_wide_kernel<16, 4>, dim3(tiles * Z), dim3(256), size_t(hidden) * 16 * 4, st, 
-        c, hn_cache, W, bias, v_begin, v_count, hidden, am_val, am_idx, logits_out, ld_logits);
+    launch_pdl(lmhead_f32_wide_kernel<16, 4>, dim3(tiles * Z), dim3(256), size_t(hidden) * 16 * 4, st, c, hn_cache, W,
+               bias, v_begin, v_count, hidden, am_val, am_idx, logits_out, ld_logits);
   }
 }
 

@@ -387,6 +387,10 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
     launch_residual_norm<T>(ctx, max_rows, h->x, h->part, ly.o.splits, h->H, xn, nullptr, h->H, h->cfg.rms_eps, st);
     prof_mark(h, 4);
     gemm(ly.gu, xn, ad ? &ad->xn : nullptr);
+    // (measured slower and not kept: the SwiGLU fused into the decode down
+    // GEMV's staging, recomputed by each of its 448 CTAs, 0.99 -> 1.10 ms per
+    // c2 decode step; the attention page combine fused into the page kernel as
+    // a last-arrival merge, 1.007 -> 1.041 ms)
     prof_mark(h, 7);
     launch_swiglu<T>(ctx, max_rows, h->part, ly.gu.splits, ly.gu.N, act, h->I, st);
     prof_mark(h, 5);
@@ -408,6 +412,7 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
 
 int launches_per_pass(const ps_handle* h) {
   if (h->mega) return 1 + (keyed(h) ? 1 : 0);
+  // embed; per layer QKV, finalize, attention, combine, O, norm, GU, SwiGLU, D, norm; LM head, argmax
   return 1 + 10 * h->L + 2;
 }
 
@@ -550,7 +555,7 @@ void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
 // decode == true: 1-row step whose token is the previous row's argmax; the
 // step advances ctx->n0 on the device (bf16: inside the LM-head kernel).
 void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode = false) {
-  h->stats.launches += launches_per_pass(h);
+  h->stats.launches += launches_per_pass(h) + (decode && !h->bf16 ? 1 : 0);
   if (h->bf16) {
     enqueue_pass_bf16(h, ctx, max_rows, tok_in, max_pos, decode);
   } else {
@@ -632,7 +637,7 @@ int capture_decode_graph(ps_handle* h) {
   if (h->graph) return PS_OK;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1, true);
-  h->stats.launches -= launches_per_pass(h);  // capture is not a launch; replays are counted
+  h->stats.launches -= launches_per_pass(h) + (h->bf16 ? 0 : 1);  // capture is not a launch (fp32: + advance); replays are counted
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
   if (e != cudaSuccess) return fail(PS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(e));
@@ -662,7 +667,7 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   for (int i = 0; i < steps; ++i) {
     if (h->graph) {
       CK(cudaGraphLaunch(h->graph, h->st));
-      h->stats.launches += launches_per_pass(h);
+      h->stats.launches += launches_per_pass(h) + (h->bf16 ? 0 : 1);
     } else {
       enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1, true);
     }
