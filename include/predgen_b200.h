@@ -97,9 +97,13 @@ int ps_verify_greedy(ps_handle* h, const int32_t* prompt, int32_t n_prompt, cons
                      float* gpu_ms);
 
 /* Fused top-k verify: the greedy pass, then the rank of every candidate token
- * in its row, rank = #{j : s_j > s_t or (s_j == s_t and j < t)} over the fp32
+ * in its row, rank = #{j : s_j > s_t or (s_j == s_t and j < t)} in the fp32
  * logits the pass's LM head produced (no sort, no host rows); k = the longest
  * prefix of cand whose ranks are < topk. KV rolled back to len(prompt)+k.
+ * bf16 with topk <= 8 and a pass of 2..160 rows: the LM epilogue keeps each
+ * (vocab tile, row)'s best topk (value, id) and the pass merges them — no
+ * logits rows exist — so a rank >= topk reads topk (the verifier only asks
+ * rank < topk). Otherwise ranks are counted exactly over materialised rows.
  * rank_out (nullable) gets the n_cand ranks; the other outputs are as in
  * ps_verify_greedy. topk == 1 accepts exactly what ps_verify_greedy accepts.
  * Unsupported (PS_ERR_UNSUPPORTED) on a vocab-sharded LM head.

@@ -166,6 +166,15 @@ struct MegaParams {
   unsigned* bar2;           // wide passes: attention-merge sync counter (one arrival per CTA per layer)
   int lm_only;              // 1: LM head + argmax over resident rows [n0, n0+rows) only (hn / rstd caches)
   float* logits_out;        // optional fp32 logits [rows][ld_logits] from the LM epilogue
+  // fused top-k verification (wide passes of <= kTopkRows rows): the LM epilogue
+  // writes each (tile, row)'s best L = topk_list (value, id) in the (-score, id)
+  // order of topk_tokens (lm.py:139-145); FINAL merges them per row and writes
+  // rank_pos[n0 + t] = rank of tokens_dev[n0 + t + 1] in row t, or L when it
+  // is not among the best L (the verifier's k: rank < k is all it asks)
+  int topk_list;            // 0: off; else L (1..kTopkList)
+  float* tk_val;            // [LM tiles][kTopkRows][kTopkList]
+  int* tk_idx;
+  int* rank_pos;            // [max_seq + kMaxWindow]
   int ld_logits;
   unsigned long long* trace;  // optional [nphases][G][12] globaltimer stamps
   int pre_max;              // weight stages issued ahead of a phase barrier (<= stages)
@@ -176,6 +185,8 @@ struct MegaParams {
 // passes one unit buffer of bf16 K, V [64][hd+8] and q [4 * grp][hd+8]
 // wide passes: K and V only (q fragments are read from global memory); a
 // buffer also holds the staged RMSNorm partials of up to kRstdStageRows rows
+constexpr int kTopkList = 8;    // fused top-k: list length per (LM tile, row); k <= kTopkList
+constexpr int kTopkRows = 160;  // fused top-k: pass widths whose LM tiles all use the vectorised epilogue
 constexpr int kRstdStageRows = 80;
 __host__ __device__ inline int mega_attn_buf_wide(int hd, int H) {
   const int kv = 2 * kPage * (hd + 8) * 2, rs = 4 * (H / 128) * kRstdStageRows * 4;

@@ -1071,6 +1071,56 @@ struct DefTile {
   int tile, c_first, npieces, r_lo, r_hi, slot0;
 };
 
+// (v, id) ahead of (v2, id2) in the (-score, id) order of topk_tokens (lm.py:139-145)
+__device__ __forceinline__ bool tk_before(float v, int i, float v2, int i2) { return v > v2 || (v == v2 && i < i2); }
+__device__ __forceinline__ void tk_cswap(float& va, int& ia, float& vb, int& ib) {
+  if (tk_before(vb, ib, va, ia)) {
+    const float tv = va;
+    const int ti = ia;
+    va = vb;
+    ia = ib;
+    vb = tv;
+    ib = ti;
+  }
+}
+
+// Fused top-k (wide LM epilogue): the best L = P.topk_list (value, id) of one row's
+// 128 logits of one LM tile (4 per lane), best first, into tk_val / tk_idx.
+// Each lane sorts its 4; every round the warp's (max, lowest id) head is
+// selected (a total order: ties cannot split) and popped by its owner.
+__device__ __forceinline__ void warp_topl(const MegaParams& P, int tile, int t, float (&v)[4], int (&id)[4], int lane) {
+  tk_cswap(v[0], id[0], v[1], id[1]);
+  tk_cswap(v[2], id[2], v[3], id[3]);
+  tk_cswap(v[0], id[0], v[2], id[2]);
+  tk_cswap(v[1], id[1], v[3], id[3]);
+  tk_cswap(v[1], id[1], v[2], id[2]);
+  float mv = -INFINITY;
+  int mi = 0x7fffffff;
+  const int L = P.topk_list;
+#pragma unroll
+  for (int r = 0; r < kTopkList; ++r) {
+    if (r >= L) break;
+    float hv = v[0];
+    int hi = id[0];
+    warp_argmax(hv, hi);
+    if (id[0] == hi) {  // owner pops its head
+      v[0] = v[1]; id[0] = id[1];
+      v[1] = v[2]; id[1] = id[2];
+      v[2] = v[3]; id[2] = id[3];
+      v[3] = -INFINITY; id[3] = 0x7fffffff;
+    }
+    if (lane == r) {
+      mv = hv;
+      mi = hi;
+    }
+  }
+  if (lane < L) {
+    const size_t o = (size_t(tile) * kTopkRows + t) * kTopkList + lane;
+    P.tk_val[o] = mv;
+    P.tk_idx[o] = mi;
+  }
+}
+
 // One row t of the vectorised finishing math: features 4*lane .. +3 of
 // `tile` (acc = their fp32 sums, X = the row's residual / RoPE inputs).
 template <class ES>
@@ -1150,14 +1200,21 @@ __device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, in
     const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
     float bv = -INFINITY;
     int bi = 0x7fffffff;
+    float tv[4];
+    int ti[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+      tv[e] = -INFINITY;
+      ti[e] = 0x7fffffff;
       if (n + e < P.vocab_local) {
         const float lv = epi_scale_bias(a4[e], rs, P.lm_bias[P.v_begin + n + e]);
         if (P.logits_out) P.logits_out[size_t(t) * P.ld_logits + n + e] = lv;
         argmax_merge(bv, bi, lv, P.v_begin + n + e);
+        tv[e] = lv;
+        ti[e] = P.v_begin + n + e;
       }
     }
+    if (P.topk_list) warp_topl(P, tile, t, tv, ti, lane);
     warp_argmax(bv, bi);
     if (lane == 0) argmax_merge(es.am_v[w][t], es.am_i[w][t], bv, bi);
   }
@@ -1530,6 +1587,81 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
 #pragma unroll
           for (int u = 0; u < 8; ++u) argmax_merge(bv, bi, vv[u], ii[u]);
           warp_argmax(bv, bi);
+          if (kWide && P.topk_list) {
+            // best L of the row over every LM tile's list: lane takes tiles
+            // lane, lane + 32, ... (heads of four requested at once) into a
+            // sorted local list, then the warp selects heads as in warp_topl;
+            // the rank of the row's next token is its position there (L: not
+            // among them)
+            const int L = P.topk_list;
+            const int ntl = (P.vocab_local + 127) / 128;
+            float lv[kTopkList];
+            int li[kTopkList];
+#pragma unroll
+            for (int k = 0; k < kTopkList; ++k) {
+              lv[k] = -INFINITY;
+              li[k] = 0x7fffffff;
+            }
+            auto worst = [&](float& v, int& i) {  // lv[L - 1], li[L - 1]
+              v = lv[0];
+              i = li[0];
+#pragma unroll
+              for (int k = 1; k < kTopkList; ++k)
+                if (k < L) {
+                  v = lv[k];
+                  i = li[k];
+                }
+            };
+            for (int tl0 = lane; tl0 < ntl; tl0 += 32 * 4) {
+              float hv[4];
+              int hi[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int tl = tl0 + 32 * u;
+                const size_t o = (size_t(tl) * kTopkRows + t) * kTopkList;
+                hv[u] = tl < ntl ? __ldcg(P.tk_val + o) : -INFINITY;
+                hi[u] = tl < ntl ? __ldcg(P.tk_idx + o) : 0x7fffffff;
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const size_t o = (size_t(tl0 + 32 * u) * kTopkRows + t) * kTopkList;
+                float v = hv[u];
+                int i = hi[u];
+                for (int k = 0; k < L; ++k) {  // tile lists are sorted: stop at the first that misses
+                  if (k > 0) {
+                    v = __ldcg(P.tk_val + o + k);
+                    i = __ldcg(P.tk_idx + o + k);
+                  }
+                  float wv;
+                  int wi;
+                  worst(wv, wi);
+                  if (!tk_before(v, i, wv, wi)) break;
+#pragma unroll
+                  for (int q = 0; q < kTopkList; ++q) tk_cswap(lv[q], li[q], v, i);  // insert, shifting down
+                }
+              }
+            }
+            const int tok = __ldcg(P.tokens_dev + n0 + t + 1);
+            int rank = L;
+#pragma unroll
+            for (int r = 0; r < kTopkList; ++r) {
+              if (r >= L) break;
+              float hv = lv[0];
+              int hi = li[0];
+              warp_argmax(hv, hi);
+              if (li[0] == hi) {
+#pragma unroll
+                for (int q = 0; q + 1 < kTopkList; ++q) {
+                  lv[q] = lv[q + 1];
+                  li[q] = li[q + 1];
+                }
+                lv[kTopkList - 1] = -INFINITY;
+                li[kTopkList - 1] = 0x7fffffff;
+              }
+              if (hi == tok && rank == L) rank = r;
+            }
+            if (lane == 0) P.rank_pos[n0 + t] = rank;
+          }
           if (lane == 0) {
             P.argmax_pos[n0 + t] = bi;
             if (P.keys) {

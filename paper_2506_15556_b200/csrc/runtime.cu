@@ -197,6 +197,15 @@ struct ps_handle {
   // LM-head re-run); cap_n0 / cap_rows = the positions the last chunk covered
   bool capture_logits = false;
   int cap_n0 = -1, cap_rows = 0;
+  // fused top-k (bf16): wide passes of 2..tk_rows_max rows keep per-(LM tile,
+  // row) best-kTopkList lists instead of logits; tk_n0 / tk_rows = the positions
+  // whose ranks the last such pass wrote into rank_pos
+  bool topk_fused = false;
+  int topk_k = 0;  // list length of fused top-k passes (the verifier's k <= kTopkList)
+  int tk_rows_max = 0, tk_n0 = -1, tk_rows = 0;
+  float* tk_val = nullptr;
+  int* tk_idx = nullptr;
+  int* rank_pos = nullptr;
   // bf16 chain state
   float* rstd = nullptr;        // [kMaxWindow] rstd of the current residual rows
   float* rstd_cache = nullptr;  // [seq_rows] rstd of the final hidden per position
@@ -502,8 +511,17 @@ void enqueue_mega(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, b
   P.bar = h->mega_cnt;
   P.bar2 = h->mega_cnt + 2;
   P.lm_only = lm_only ? 1 : 0;
-  P.logits_out = (logits_out == nullptr && h->capture_logits && !lm_only) ? h->logits_buf : logits_out;
+  const bool tk = h->topk_fused && max_rows >= 2 && max_rows <= h->tk_rows_max && h->cfg.vocab_shards == 1;
+  P.logits_out = (logits_out == nullptr && h->capture_logits && !lm_only && !tk) ? h->logits_buf : logits_out;
   P.ld_logits = h->v_count;
+  P.topk_list = tk ? h->topk_k : 0;
+  P.tk_val = h->tk_val;
+  P.tk_idx = h->tk_idx;
+  P.rank_pos = h->rank_pos;
+  if (tk) {
+    h->tk_n0 = -2;  // set by the caller (the pass's first position is device-side)
+    h->tk_rows = max_rows;
+  }
   P.trace = h->mega_trace;
   {
     // L2 prefetch depth (weight boxes per CTA beyond the smem ring) for the
@@ -592,6 +610,7 @@ int enqueue_extend(ps_handle* h, const int* tokens, int n, int* base_out) {
       h->cap_n0 = base + done;
       h->cap_rows = rows;
     }
+    if (h->tk_n0 == -2) h->tk_n0 = base + done;  // this pass wrote fused top-k ranks
     h->stats.passes += 1;
     h->stats.rows += rows;
     done += rows;
@@ -922,6 +941,8 @@ int ps_create(const ps_config* cfg, ps_handle** out) {
     // per-phase counter block: one counter per tile plus the all-split
     // phases' grid-sync counter at index `tiles` (megakernel.cu)
     h->mega_max_tiles = (std::max(std::max(h->qd + 2 * h->kvd, 2 * h->I), std::max(h->H, h->v_count)) + 127) / 128 + 1;
+    // fused top-k needs every LM tile on the vectorised epilogue (rows * 512 <= 2 * attention buffer)
+    h->tk_rows_max = std::min(kTopkRows, mega_attn_buf_wide(h->hd, h->H) / 256);
     h->mega_cnt_words = 64 + size_t(3 + 5 * h->L) * h->mega_max_tiles;
     h->mega_cnt = h->dalloc<unsigned>(h->mega_cnt_words);
     h->d_wmaps = h->dalloc<CUtensorMap>(size_t(4) * h->L + 1);
@@ -996,6 +1017,9 @@ void ps_destroy(ps_handle* h) {
   for (void* p : h->allocs) cudaFree(p);
   for (void* p : h->host_allocs) cudaFreeHost(p);
   if (h->logits_buf) cudaFree(h->logits_buf);
+  if (h->tk_val) cudaFree(h->tk_val);
+  if (h->tk_idx) cudaFree(h->tk_idx);
+  if (h->rank_pos) cudaFree(h->rank_pos);
   if (h->nccl_comm) nccl_api()->comm_destroy(h->nccl_comm);
   if (h->st) cudaStreamDestroy(h->st);
   delete h->prof;
@@ -1029,14 +1053,14 @@ namespace {
 // same LM-head arithmetic the passes used (bf16: the megakernel's LM phase in
 // LM-only mode; fp32: lmhead_f32_kernel), so every value is the one the device
 // argmax saw. rows <= kMaxWindow. Enqueued on h->st.
-int enqueue_logits_rows(ps_handle* h, int first, int rows) {
-  if (!h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
+int enqueue_logits_rows(ps_handle* h, int first, int rows, bool write_logits = true) {
+  if (write_logits && !h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
   int slot;
   PassCtx* hc = next_ctx_slot(h, &slot);
   *hc = PassCtx{first, rows, 0, 0, 0, {0, 0, 0}};
   CK(copy_async(h, h->d_ctx_aux, hc, sizeof(PassCtx), cudaMemcpyHostToDevice));
   if (h->bf16) {
-    enqueue_mega(h, h->d_ctx_aux, rows, nullptr, false, true, h->logits_buf);
+    enqueue_mega(h, h->d_ctx_aux, rows, nullptr, false, true, write_logits ? h->logits_buf : nullptr);
   } else {
     launch_lmhead_f32(h->d_ctx_aux, rows, static_cast<const float*>(h->hn_cache), 0,
                       static_cast<const float*>(h->head), h->lm_bias, h->v_begin, h->v_count, h->H, h->am_val,
@@ -1065,12 +1089,24 @@ int verify_impl(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int
   const int n = int(seq.size());
   int computed = 0, base = 0;
   bool enq = false;
+  // bf16, k <= kTopkList: ranks from the fused per-tile lists (no logits rows)
+  const bool fused_topk = topk > 0 && topk <= kTopkList && h->bf16 && h->tk_rows_max >= 2;
+  if (fused_topk && !h->tk_val) {
+    const size_t n_tk = size_t(h->am_tiles) * kTopkRows * kTopkList;
+    CK(cudaMalloc(&h->tk_val, sizeof(float) * n_tk));
+    CK(cudaMalloc(&h->tk_idx, sizeof(int) * n_tk));
+    CK(cudaMalloc(&h->rank_pos, sizeof(int) * (size_t(h->cfg.max_seq) + kMaxWindow)));
+  }
   if (topk > 0 && !h->logits_buf) CK(cudaMalloc(&h->logits_buf, sizeof(float) * size_t(kMaxWindow) * h->v_count));
   CK(cudaEventRecord(h->ev0, h->st));
   h->capture_logits = topk > 0;
+  h->topk_fused = fused_topk;
+  h->topk_k = topk;
   h->cap_n0 = -1;
+  h->tk_n0 = -1;
   const int sync_rc = sync_to(h, seq.data(), n, &computed, &base, &enq, false);
   h->capture_logits = false;
+  h->topk_fused = false;
   if (sync_rc) return sync_rc;
   if (n_cand) {
     int slot;
@@ -1089,14 +1125,25 @@ int verify_impl(ps_handle* h, const int32_t* prompt, int32_t n_prompt, const int
     h->stats.launches += 1;
     if (topk > 0) {  // rows n_prompt-1 .. n_prompt+n_cand-2 score the candidate tokens
       const int first = n_prompt - 1;
-      const float* rows = h->logits_buf;
-      if (enq && h->cap_n0 >= 0 && h->cap_n0 <= first && first + n_cand <= h->cap_n0 + h->cap_rows) {
-        rows = h->logits_buf + size_t(first - h->cap_n0) * h->v_count;  // written by this very pass
-      } else {  // rows resident from an earlier pass (or a chunked extend): LM head over them
-        if (int rc = enqueue_logits_rows(h, first, n_cand)) return rc;
+      const bool pass_ranked = enq && h->tk_n0 >= 0 && h->tk_n0 <= first && first + n_cand <= h->tk_n0 + h->tk_rows;
+      if (fused_topk && (pass_ranked || (n_cand >= 2 && n_cand <= h->tk_rows_max))) {
+        if (!pass_ranked) {  // rows resident from an earlier pass: LM head over them, lists only
+          h->topk_fused = true;
+          const int rc = enqueue_logits_rows(h, first, n_cand, false);
+          h->topk_fused = false;
+          if (rc) return rc;
+        }
+        CK(cudaMemcpyAsync(h->d_res + 4, h->rank_pos + first, sizeof(int) * n_cand, cudaMemcpyDeviceToDevice, h->st));
+      } else {
+        const float* rows = h->logits_buf;
+        if (enq && h->cap_n0 >= 0 && h->cap_n0 <= first && first + n_cand <= h->cap_n0 + h->cap_rows) {
+          rows = h->logits_buf + size_t(first - h->cap_n0) * h->v_count;  // written by this very pass
+        } else {  // rows resident from an earlier pass (or a chunked extend): LM head over them
+          if (int rc = enqueue_logits_rows(h, first, n_cand)) return rc;
+        }
+        launch_topk_rank(rows, h->v_count, h->v_count, h->d_cand, n_cand, h->d_res + 4, h->st);
+        h->stats.launches += 1;
       }
-      launch_topk_rank(rows, h->v_count, h->v_count, h->d_cand, n_cand, h->d_res + 4, h->st);
-      h->stats.launches += 1;
     }
     CK(copy_async(h, h->h_res, h->d_res, sizeof(int) * (topk > 0 ? 4 + n_cand : 2), cudaMemcpyDeviceToHost));
   }

@@ -16,7 +16,7 @@ import pytest
 
 from conftest import GOLDEN
 from paper_2506_15556_b200 import B200LM, PipelineConfig, make_stream, run_turn, specstream
-from paper_2506_15556_b200.shapes import TINY, small_shape
+from paper_2506_15556_b200.shapes import MODE_BF16, TINY, small_shape
 from paper_2506_15556_b200.fused import verify_greedy, verify_topk
 
 pytestmark = pytest.mark.gpu
@@ -58,15 +58,38 @@ def test_topk_known_answer_and_ranks(lm):
         order = sorted(range(len(row)), key=lambda i: (-row[i], i))
         cand.append(int(order[r]))
         assert rank_of(row, cand[-1]) == r
-    for k in (1, 2, 3, 5, 7):
+    for k in (1, 2, 3, 5, 7, 9):
         d = lm.verify_topk_detail(prompt, cand, k)
-        assert d["rank"] == want_ranks
+        # bf16, k <= 8: ranks from the fused best-k lists, exact below k and k past it
+        fused = lm.shape.mode == MODE_BF16 and k <= 8
+        assert d["rank"] == ([min(r, k) for r in want_ranks] if fused else want_ranks)
         expect = next((i for i, r in enumerate(want_ranks) if r >= k), len(cand))
         assert d["k"] == expect, (k, d["k"], expect)
         # the KV was rolled back to |P| + k
         assert lm.resident() == prompt + cand[:expect]
     g = lm.verify_greedy_detail(prompt, cand)
     assert g["k"] == lm.verify_topk_detail(prompt, cand, 1)["k"]
+
+
+def test_fused_topk_lists_rank_wide_window(lm):
+    """One wide verify pass (bf16: ranks from the per-tile best-k lists merged
+    in FINAL, no logits rows; fp32: counted over materialised rows): a rank
+    below k is exact, anything else reads k on the bf16 path."""
+    rng = np.random.default_rng(4)
+    vocab = lm.vocab_size
+    prompt = [int(t) for t in rng.integers(4, vocab, 24)]
+    want = [int(r) for r in rng.choice([0, 1, 2, 5, 7, 8, 9, 30, 500], size=40)]
+    cand = []
+    for r in want:
+        block, _, _ = lm.forward(prompt + cand)
+        row = np.asarray(block.row_for(len(prompt) + len(cand) - 1), dtype=np.float32)
+        order = sorted(range(len(row)), key=lambda i: (-row[i], i))
+        cand.append(int(order[r]))
+    lm.truncate(len(prompt) - 6)  # the verify pass recomputes 6 prompt rows + the 40 candidate rows
+    d = lm.verify_topk_detail(prompt, cand, 8)
+    cap = 8 if lm.shape.mode == MODE_BF16 else None
+    assert d["rank"] == [min(r, cap) if cap else r for r in want]
+    assert d["k"] == next((i for i, r in enumerate(want) if r >= 8), len(cand))
 
 
 def test_topk_verifier_fused_equals_generic(lm):
