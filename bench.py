@@ -178,8 +178,12 @@ class CpuPassTimer:
 
     def __init__(self, shape, threads: int, context: int = 128):
         import numpy as np
+        from threadpoolctl import threadpool_limits
         from oracle.decoder import DecoderOracle
 
+        # torchrun exports OMP_NUM_THREADS=1 to every rank, which OpenBLAS read at load
+        # time: set the BLAS pool to the thread count this timer reports
+        self._limits = threadpool_limits(limits=threads, user_api="blas")
         t0 = time.perf_counter()
         d = dict(shape.as_dict())
         d["mode"] = 0  # fp32 arithmetic: no bf16 rounding emulation in the timed port
