@@ -75,6 +75,15 @@ __global__ void __launch_bounds__(192) probe(unsigned* bar, unsigned* flags, flo
         }
         seen = 1;
       }
+    } else if (V == 6) {  // arrival counter + generation flag in another line (pollers never touch the counter)
+      if (threadIdx.x == 0) {
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == unsigned(G) * it - 1) st_rel(flags, it);
+        else
+          while (ld_acq(flags) < unsigned(it)) {
+          }
+      }
     } else if (V == 5) {  // two loads in flight per poll round
       if (threadIdx.x == 0) {
         red_rel(bar);
@@ -118,18 +127,20 @@ int main() {
   cudaMalloc(&scratch, size_t(148) * 16384 * 4);
   const char* names[] = {"red.release + ld.acquire poll", "fence + red.relaxed + relaxed poll + fence",
                          "red.release + relaxed poll + fence", "per-CTA flags, warp polls all",
-                         "red.release, 3 pollers", "2 relaxed loads in flight + fence"};
+                         "red.release, 3 pollers", "2 relaxed loads in flight + fence",
+                         "atom.acq_rel + generation flag"};
   for (int wf : {0, 1024, 4096, 16384}) {
     for (int rep = 0; rep < 2; ++rep) {
-      float t[6];
+      float t[7];
       t[0] = run<0>(bar, flags, scratch, 4000, wf);
       t[1] = run<1>(bar, flags, scratch, 4000, wf);
       t[2] = run<2>(bar, flags, scratch, 4000, wf);
       t[3] = run<3>(bar, flags, scratch, 4000, wf);
       t[4] = run<4>(bar, flags, scratch, 4000, wf);
       t[5] = run<5>(bar, flags, scratch, 4000, wf);
+      t[6] = run<6>(bar, flags, scratch, 4000, wf);
       if (rep)
-        for (int v = 0; v < 6; ++v) printf("stores %6d B/CTA  %-45s %.3f us/barrier\n", wf * 4, names[v], t[v]);
+        for (int v = 0; v < 7; ++v) printf("stores %6d B/CTA  %-45s %.3f us/barrier\n", wf * 4, names[v], t[v]);
     }
   }
   return 0;
