@@ -418,7 +418,15 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
 // barrier, and unit i+1's loads overlap unit i's math.
 constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
 constexpr int kMaxUnitList = 32;  // units computed before their counts/merges are flushed
-constexpr int kAttnRowsW = 16;    // wide passes: query rows per unit (one 4-row M-tile per worker warp)
+// wide passes: query rows per unit (one 4-row M-tile per worker warp): 16 when
+// the pass's units fit one round over the grid, else 24 (all 6 worker warps),
+// so long contexts take fewer rounds (attention_rows_wide)
+constexpr int kAttnRowsW = 16;
+constexpr int kAttnRowsW2 = 24;
+__device__ __forceinline__ int attention_rows_wide(const MegaParams& P, int rows, int n0, int G) {
+  const int npages = (n0 + rows - 1) / kPage + 1;
+  return ((rows + kAttnRowsW - 1) / kAttnRowsW) * P.kv_heads * npages <= G ? kAttnRowsW : kAttnRowsW2;
+}
 
 struct AttnSmem {  // two unit buffers [K | V | Q] at base + b * buf
   unsigned char* base;
@@ -511,8 +519,8 @@ struct AttnUnit {
 
 // The i-th unit (i >= 0 counts only units with work) of CTA c: units are
 // dealt round-robin (u = c, c + G, ...), page fastest.
-template <int R>
-__device__ __forceinline__ AttnUnit attn_unit_from(const MegaParams& P, int rows, int n0, int u_start, int G, int& u_next) {
+__device__ __forceinline__ AttnUnit attn_unit_from(const MegaParams& P, int R, int rows, int n0, int u_start, int G,
+                                                   int& u_next) {
   const int npages = (n0 + rows - 1) / kPage + 1;
   const int nblocks = (rows + R - 1) / R;
   const int units = nblocks * P.kv_heads * npages;
@@ -611,19 +619,22 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
     for (int nt = 0; nt < 8; ++nt) S[nt][0] = S[nt][1] = S[nt][2] = S[nt][3] = 0.f;
     const uint32_t qa = qbase + uint32_t(mt * 16 + (mi & 1) * 8 + mr) * rs + uint32_t(mi >> 1) * 16;
     const uint32_t ka = kbase + uint32_t((mi >> 1) * 8 + mr) * rs + uint32_t(mi & 1) * 16;
-    for (int ks = 0; ks < hd / 16; ++ks) {
-      uint32_t a0, a1, a2, a3;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
-                   : "r"(qa + ks * 32));
 #pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
-        uint32_t b0, b1, b2, b3;
+    for (int ks = 0; ks < 8; ++ks) {  // hd / 16 <= 8 k-steps, unrolled so fragment loads run ahead
+      if (ks < hd / 16) {
+        uint32_t a0, a1, a2, a3;
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                     : "r"(ka + uint32_t(nt * 8) * rs + ks * 32));
-        mma_bf16(S[nt], a0, a1, a2, a3, b0, b1);
-        mma_bf16(S[nt + 1], a0, a1, a2, a3, b2, b3);
+                     : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                     : "r"(qa + ks * 32));
+#pragma unroll
+        for (int nt = 0; nt < 8; nt += 2) {
+          uint32_t b0, b1, b2, b3;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                       : "r"(ka + uint32_t(nt * 8) * rs + ks * 32));
+          mma_bf16(S[nt], a0, a1, a2, a3, b0, b1);
+          mma_bf16(S[nt + 1], a0, a1, a2, a3, b2, b3);
+        }
       }
     }
     if (tr && mt == 0) { float z = S[0][0] + S[7][3]; if (z == 12345.f) stamp(P, trace_p, blockIdx.x, gridDim.x, 15); stamp(P, trace_p, blockIdx.x, gridDim.x, 14); }
@@ -727,8 +738,33 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
 // softmax, hi/lo P) is attention_unit's, so results are bitwise the decode
 // step's. Page-local (O, m, l) go to o_part / ml_part; the merge runs after
 // a grid-wide sync (attn_merge_items).
+// q fragments of this warp's M-tile of unit U (pairs p0 = lane / 4, p1 = p0 + 8;
+// zero past the tile's pairs), all k-steps: requested before the unit's K / V
+// wait so the two round trips overlap
+__device__ __forceinline__ void attn_q_frags_wide(const MegaParams& P, const AttnUnit& U, int w, int lane,
+                                                  uint32_t (&qf)[8][4]) {
+  const int hd = P.hd, grp = P.heads / P.kv_heads;
+  const int r0 = U.t0 + 4 * w;
+  const int npairs = max(0, min(4, U.t1 - r0)) * grp;
+  const int g8 = lane >> 2, q4 = lane & 3;
+  const int p0 = g8, p1 = g8 + 8;
+  const bool va = U.valid && p0 < npairs, vb = U.valid && p1 < npairs;
+  const uint32_t* qa = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p0 / grp) * P.qd +
+                                                         size_t(U.kvh * grp + p0 % grp) * hd) + q4;
+  const uint32_t* qb = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p1 / grp) * P.qd +
+                                                         size_t(U.kvh * grp + p1 % grp) * hd) + q4;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const bool k_ok = ks < hd / 16;
+    qf[ks][0] = (va && k_ok) ? __ldcg(qa + ks * 8) : 0u;
+    qf[ks][1] = (vb && k_ok) ? __ldcg(qb + ks * 8) : 0u;
+    qf[ks][2] = (va && k_ok) ? __ldcg(qa + ks * 8 + 4) : 0u;
+    qf[ks][3] = (vb && k_ok) ? __ldcg(qb + ks * 8 + 4) : 0u;
+  }
+}
+
 __device__ __forceinline__ void attention_unit_wide(const MegaParams& P, const AttnUnit& U, int n0, const AttnSmem& A,
-                                                    int b, int w, int lane) {
+                                                    int b, int w, int lane, const uint32_t (&qf)[8][4]) {
   const int hd = P.hd, grp = P.heads / P.kv_heads;
   const int r0 = U.t0 + 4 * w;
   const int nr = min(4, U.t1 - r0);
@@ -741,23 +777,6 @@ __device__ __forceinline__ void attention_unit_wide(const MegaParams& P, const A
   const int g8 = lane >> 2, q4 = lane & 3;
   const int mi = lane >> 3, mr = lane & 7;
   const int p0 = g8, p1 = g8 + 8;
-  // q fragments of pairs p0 / p1 (zero past npairs), all k-steps up front
-  uint32_t qf[8][4];
-  {
-    const uint32_t* qa = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p0 / grp) * P.qd +
-                                                           size_t(kvh * grp + p0 % grp) * hd) + q4;
-    const uint32_t* qb = reinterpret_cast<const uint32_t*>(P.q + size_t(r0 + p1 / grp) * P.qd +
-                                                           size_t(kvh * grp + p1 % grp) * hd) + q4;
-    const bool va = p0 < npairs, vb = p1 < npairs;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const bool k_ok = ks < hd / 16;
-      qf[ks][0] = (va && k_ok) ? __ldcg(qa + ks * 8) : 0u;
-      qf[ks][1] = (vb && k_ok) ? __ldcg(qb + ks * 8) : 0u;
-      qf[ks][2] = (va && k_ok) ? __ldcg(qa + ks * 8 + 4) : 0u;
-      qf[ks][3] = (vb && k_ok) ? __ldcg(qb + ks * 8 + 4) : 0u;
-    }
-  }
   float S[8][4];
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) S[nt][0] = S[nt][1] = S[nt][2] = S[nt][3] = 0.f;
@@ -1535,6 +1554,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
       stamp(P, 0, c, G, 2);
       grid_arrive(P.bar);
     }
+    const int rw = kWide ? attention_rows_wide(P, rows, n0, G) : kAttnRows;  // attention unit rows
     for (int p = p_first; p < nphases; ++p) {
       const int kind = phase_kind(p, P.L);
       const int layer = kind == PH_LM ? P.L - 1 : (p - 1) / 5;
@@ -1556,7 +1576,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
         // keys cached by earlier passes for this CTA's first attention unit of
         // the layer: requested now, consumed after the next barrier
         int un = 0;
-        const AttnUnit U0 = attn_unit_from<kWide ? kAttnRowsW : kAttnRows>(P, rows, n0, c, G, un);
+        const AttnUnit U0 = attn_unit_from(P, kWide ? rw : kAttnRows, rows, n0, c, G, un);
         if (U0.valid) attn_issue<kWide>(P, layer, U0, n0, A, 0, 0, tid);
         if (U0.valid || rstd_pending) cp_async_commit();  // (the staged partials are the group before)
       }
@@ -1679,12 +1699,12 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
         // units (kv head, page, 16-row block), double-buffered K/V; the first
         // unit's cached keys were requested in the QKV phase
         int un = 0, un2 = 0;
-        AttnUnit cur = attn_unit_from<kAttnRowsW>(P, rows, n0, c, G, un);
+        AttnUnit cur = attn_unit_from(P, rw, rows, n0, c, G, un);
         AttnUnit nxt{0, 0, 0, 0, false};
         if (cur.valid) {
           attn_issue<kWide>(P, layer, cur, n0, A, 0, 1, tid);
           cp_async_commit();
-          nxt = attn_unit_from<kAttnRowsW>(P, rows, n0, un, G, un2);
+          nxt = attn_unit_from(P, rw, rows, n0, un, G, un2);
           if (nxt.valid) {
             attn_issue<kWide>(P, layer, nxt, n0, A, 1, 0, tid);
             attn_issue<kWide>(P, layer, nxt, n0, A, 1, 1, tid);
@@ -1692,15 +1712,17 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
           cp_async_commit();
         }
         for (int i = 0; cur.valid; ++i) {
+          uint32_t qf[8][4];
+          attn_q_frags_wide(P, cur, w, lane, qf);
           cp_async_wait<1>();
           wk_bar();
           if (tid == 0 && i == 0) stamp(P, p, c, G, 7);
-          attention_unit_wide(P, cur, n0, A, i & 1, w, lane);
+          attention_unit_wide(P, cur, n0, A, i & 1, w, lane, qf);
           wk_bar();  // buffer i&1 is free again
           if (tid == 0 && i == 0) stamp(P, p, c, G, 9);
           AttnUnit nn{0, 0, 0, 0, false};
           int un3 = un2;
-          if (nxt.valid) nn = attn_unit_from<kAttnRowsW>(P, rows, n0, un2, G, un3);
+          if (nxt.valid) nn = attn_unit_from(P, rw, rows, n0, un2, G, un3);
           if (nn.valid) {
             attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 0, tid);
             attn_issue<kWide>(P, layer, nn, n0, A, i & 1, 1, tid);
@@ -1727,7 +1749,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
         // frees deepens the weight ring); the first unit's cached keys were
         // requested in the QKV phase
         int un = 0;
-        AttnUnit cur = attn_unit_from<kAttnRows>(P, rows, n0, c, G, un);
+        AttnUnit cur = attn_unit_from(P, kAttnRows, rows, n0, c, G, un);
         for (int i = 0; cur.valid; ++i) {
           if (i > 0) attn_issue<kWide>(P, layer, cur, n0, A, 0, 0, tid);
           attn_issue<kWide>(P, layer, cur, n0, A, 0, 1, tid);
@@ -1745,7 +1767,7 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
           wk_bar();
           attn_count_merge(P, n0, 1, w, lane, es);  // ends with wk_bar
           int un2 = un;
-          cur = attn_unit_from<kAttnRows>(P, rows, n0, un, G, un2);
+          cur = attn_unit_from(P, kAttnRows, rows, n0, un, G, un2);
           un = un2;
         }
       } else {
