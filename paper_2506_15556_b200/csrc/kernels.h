@@ -69,6 +69,12 @@ void launch_attention(const PassCtx* ctx, int max_rows, int max_pos, const T* q,
                       const T* vpool, const int* page_table, KvGeom g, int layer, int heads,
                       float* o_part, float* ml_part, T* attn_out, cudaStream_t st);
 
+// 1-row passes: qkv_finalize + attention_page fused (CTA = kv head x page), then the combine
+void launch_qkv_attention_decode(const PassCtx* ctx, int max_pos, const float* part, int splits, int N,
+                                 const float* bias, const float2* rope, float* kpool, float* vpool,
+                                 const int* page_table, KvGeom g, int layer, int heads, float* o_part,
+                                 float* ml_part, float* attn_out, cudaStream_t st);
+
 template <typename T>
 void launch_residual_norm(const PassCtx* ctx, int max_rows, float* x, const float* part, int splits,
                           int ldp, T* xn, T* hn_cache, int hidden, float eps, cudaStream_t st);

@@ -207,6 +207,113 @@ __global__ void attention_combine_kernel(const PassCtx* __restrict__ ctx, int he
   out[size_t(t) * heads * hd + size_t(h) * hd + d] = from_f32<T>(f32_attn_combine(o_part, ml_part, base, nsplit, hd, d));
 }
 
+// Decode steps (1 row): qkv_finalize and attention_page in one launch. CTA =
+// (kv head, page) as attention_page_kernel's; every CTA finalises the q of
+// its GQA group itself (split-K sum + bias + RoPE: qkv_finalize's arithmetic,
+// so q is bitwise the same), and the CTA of the row's last page also
+// finalises the step's k / v and appends them to the paged cache before
+// staging that page (no other CTA reads them). One kernel and one global
+// round trip less per layer than the separate pair.
+__global__ void __launch_bounds__(512) qkv_attention_decode_kernel(
+    const PassCtx* __restrict__ ctx, const float* __restrict__ part, int splits, int N, const float* __restrict__ bias,
+    const float2* __restrict__ rope, float* __restrict__ kpool, float* __restrict__ vpool,
+    const int* __restrict__ page_table, KvGeom g, int layer, int heads, int max_splits, float scale,
+    float* __restrict__ o_part, float* __restrict__ ml_part) {
+  pdl_enter();
+  extern __shared__ float sm[];
+  const int kvh = blockIdx.x, s = blockIdx.y;
+  if (ctx->stop || ctx->rows < 1) return;
+  const int pos = ctx->n0;  // row t = 0
+  if (s > pos / kPage) return;
+  const int hd = g.head_dim, half = hd >> 1, grp = heads / g.kv_heads;
+  const int nkeys = min(kPage, pos + 1 - s * kPage);
+  float* Ks = sm;                     // [64][hd+1]
+  float* Vs = Ks + kPage * (hd + 1);  // [64][hd]
+  float* Qs = Vs + kPage * hd;        // [grp][hd]
+  const size_t sstride = size_t(kMaxWindow) * N;
+  auto sum_col = [&](int c) {
+    float v = f32_sum_splits(part + c, splits, sstride);
+    if (bias) v += bias[c];
+    return v;
+  };
+  const size_t page = size_t(page_table[s]);
+  const size_t off = size_t(layer) * g.layer_stride() + (page * g.kv_heads + kvh) * kPage * hd;
+  const bool last = s == pos / kPage;
+  // q of the group's heads (pairs), and on the last page the step's k / v
+  const int nqp = grp * half, nkp = last ? half : 0, nv = last ? half : 0;
+  for (int p = threadIdx.x; p < nqp + nkp + nv; p += blockDim.x) {
+    if (p < nqp + nkp) {
+      const bool is_q = p < nqp;
+      const int pp = is_q ? p : p - nqp;
+      const int h = pp / half, i = pp % half;  // (local head for q)
+      const int col = is_q ? (kvh * grp + h) * hd + i : heads * hd + kvh * hd + i;
+      float ra, rb;
+      f32_rope(sum_col(col), sum_col(col + half), rope[size_t(pos) * half + i], ra, rb);
+      if (is_q) {
+        Qs[h * hd + i] = ra;
+        Qs[h * hd + i + half] = rb;
+      } else {
+        float* kr = kpool + off + size_t(pos % kPage) * hd;
+        kr[i] = ra;
+        kr[i + half] = rb;
+      }
+    } else {
+      const int i = p - nqp - nkp;
+      const int col = (heads + g.kv_heads) * hd + kvh * hd + i;
+      float* vr = vpool + off + size_t(pos % kPage) * hd;
+      vr[i] = sum_col(col);
+      vr[i + half] = sum_col(col + half);
+    }
+  }
+  __syncthreads();  // the appended k / v row is read back below (L2 loads, same CTA)
+  const int n4 = nkeys * hd / 4;
+  for (int e0 = threadIdx.x; e0 < n4; e0 += blockDim.x * 4) {
+    float4 kv[4], vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + int(blockDim.x) * u;
+      if (e < n4) {
+        kv[u] = __ldcg(reinterpret_cast<const float4*>(kpool + off) + e);
+        vv[u] = __ldcg(reinterpret_cast<const float4*>(vpool + off) + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + int(blockDim.x) * u;
+      if (e < n4) {
+        const int j = (4 * e) / hd, d = (4 * e) % hd;
+        float* kr = Ks + j * (hd + 1) + d;
+        kr[0] = kv[u].x; kr[1] = kv[u].y; kr[2] = kv[u].z; kr[3] = kv[u].w;
+        *reinterpret_cast<float4*>(Vs + j * hd + d) = vv[u];
+      }
+    }
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w >= grp) return;
+  const size_t slot = (size_t(kvh * grp + w)) * max_splits + s;  // row t = 0
+  f32_attn_page_head(Qs + w * hd, Ks, Vs, hd, nkeys, scale, lane, o_part + slot * hd, ml_part + slot * 2);
+}
+
+void launch_qkv_attention_decode(const PassCtx* ctx, int max_pos, const float* part, int splits, int N,
+                                 const float* bias, const float2* rope, float* kpool, float* vpool,
+                                 const int* page_table, KvGeom g, int layer, int heads, float* o_part,
+                                 float* ml_part, float* attn_out, cudaStream_t st) {
+  const int max_splits = max_pos / kPage + 1;
+  const int grp = heads / g.kv_heads, hd = g.head_dim;
+  const size_t smem = (size_t(kPage) * (hd + 1) + size_t(kPage) * hd + size_t(grp) * hd) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(qkv_attention_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  const float scale = float(1.0 / sqrt(double(hd)));
+  launch_pdl(qkv_attention_decode_kernel, dim3(g.kv_heads, max_splits), dim3(max(grp, 4) * 32), smem, st, ctx, part,
+             splits, N, bias, rope, kpool, vpool, page_table, g, layer, heads, max_splits, scale, o_part, ml_part);
+  launch_pdl(attention_combine_kernel<float>, dim3(1, heads), dim3(hd), 0, st, ctx, heads, hd, max_splits, o_part,
+             ml_part, attn_out);
+}
+
 template <typename T>
 void launch_attention(const PassCtx* ctx, int max_rows, int max_pos, const T* q, const T* kpool,
                       const T* vpool, const int* page_table, KvGeom g, int layer, int heads,

@@ -384,12 +384,20 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
     prof_mark(h, 1);
     gemm(ly.qkv, xn, ad ? &ad->xn : nullptr);
     prof_mark(h, 7);
-    launch_qkv_finalize<T>(ctx, max_rows, h->part, ly.qkv.splits, ly.qkv.N, static_cast<const T*>(ly.bqkv), h->rope,
-                           qb, static_cast<T*>(h->kpool), static_cast<T*>(h->vpool), h->d_page_table, h->g, l, h->nh,
-                           st);
-    prof_mark(h, 2);
-    launch_attention<T>(ctx, max_rows, max_pos, qb, static_cast<const T*>(h->kpool), static_cast<const T*>(h->vpool),
-                        h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part, attn, st);
+    if (max_rows <= 1) {  // decode step: finalize + page attention in one kernel
+      launch_qkv_attention_decode(ctx, max_pos, h->part, ly.qkv.splits, ly.qkv.N, static_cast<const float*>(ly.bqkv),
+                                  h->rope, static_cast<float*>(h->kpool), static_cast<float*>(h->vpool),
+                                  h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part,
+                                  reinterpret_cast<float*>(attn), st);
+    } else {
+      launch_qkv_finalize<T>(ctx, max_rows, h->part, ly.qkv.splits, ly.qkv.N, static_cast<const T*>(ly.bqkv), h->rope,
+                             qb, static_cast<T*>(h->kpool), static_cast<T*>(h->vpool), h->d_page_table, h->g, l,
+                             h->nh, st);
+      prof_mark(h, 2);
+      launch_attention<T>(ctx, max_rows, max_pos, qb, static_cast<const T*>(h->kpool),
+                          static_cast<const T*>(h->vpool), h->d_page_table, h->g, l, h->nh, h->o_part, h->ml_part,
+                          attn, st);
+    }
     prof_mark(h, 3);
     gemm(ly.o, attn, ad ? &ad->attn : nullptr);
     prof_mark(h, 0);
@@ -419,10 +427,11 @@ void enqueue_pass_simt(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
   prof_mark(h, 7);
 }
 
-int launches_per_pass(const ps_handle* h) {
+int launches_per_pass(const ps_handle* h, int max_rows) {
   if (h->mega) return 1 + (keyed(h) ? 1 : 0);
   // embed; per layer QKV, finalize, attention, combine, O, norm, GU, SwiGLU, D, norm; LM head, argmax
-  return 1 + 10 * h->L + 2;
+  // (1-row passes: finalize + attention are one kernel)
+  return 1 + (max_rows <= 1 ? 9 : 10) * h->L + 2;
 }
 
 
@@ -573,7 +582,7 @@ void enqueue_pass_bf16(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_
 // decode == true: 1-row step whose token is the previous row's argmax; the
 // step advances ctx->n0 on the device (bf16: inside the LM-head kernel).
 void enqueue_pass_any(ps_handle* h, PassCtx* ctx, int max_rows, const int* tok_in, int max_pos, bool decode = false) {
-  h->stats.launches += launches_per_pass(h) + (decode && !h->bf16 ? 1 : 0);
+  h->stats.launches += launches_per_pass(h, max_rows) + (decode && !h->bf16 ? 1 : 0);
   if (h->bf16) {
     enqueue_pass_bf16(h, ctx, max_rows, tok_in, max_pos, decode);
   } else {
@@ -656,7 +665,7 @@ int capture_decode_graph(ps_handle* h) {
   if (h->graph) return PS_OK;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   enqueue_pass_any(h, h->d_ctx, 1, nullptr, h->cfg.max_seq - 1, true);
-  h->stats.launches -= launches_per_pass(h) + (h->bf16 ? 0 : 1);  // capture is not a launch (fp32: + advance); replays are counted
+  h->stats.launches -= launches_per_pass(h, 1) + (h->bf16 ? 0 : 1);  // capture is not a launch (fp32: + advance); replays are counted
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
   if (e != cudaSuccess) return fail(PS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(e));
@@ -686,7 +695,7 @@ int run_decode_steps(ps_handle* h, int n0, int steps, int stop_at_eos, int* exec
   for (int i = 0; i < steps; ++i) {
     if (h->graph) {
       CK(cudaGraphLaunch(h->graph, h->st));
-      h->stats.launches += launches_per_pass(h) + (h->bf16 ? 0 : 1);
+      h->stats.launches += launches_per_pass(h, 1) + (h->bf16 ? 0 : 1);
     } else {
       enqueue_pass_any(h, h->d_ctx, 1, nullptr, n0 + steps - 1, true);
     }
