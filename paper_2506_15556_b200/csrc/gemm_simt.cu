@@ -136,20 +136,30 @@ __device__ __forceinline__ void rows_x_tokens(float (&a)[R * TT], const float4* 
 // bitwise the decode GEMV's.
 // A CTA stages its TT-token chunk of x once and then walks its units j =
 // blockIdx.x, + gridDim.x, ...; a unit is U consecutive 8R-row sub-tiles.
-// Weight chunks stream through a per-warp 3-stage shared-memory ring with
-// cp.async, two chunks ahead and across sub-tile boundaries: each lane copies
+// Weight chunks stream through a per-warp kWideStages-stage shared-memory ring
+// with cp.async, kWideStages - 1 chunks ahead and across sub-tile boundaries
+// (3, 4 and 5 stages measured the same: c2 verify 4.44-4.46 ms): each lane copies
 // and later reads only its own chunks, so a per-thread wait_group is the only
 // synchronisation. (Register prefetch of the next chunk was sunk by the
 // compiler to the end of the current one, and every chunk then waited a full
 // L2/DRAM round trip.) epi(sums, first row of the warp, tt, nt) gets the two
 // sums lane l holds after the butterfly (values 2l, 2l + 1; value = i*TT + t);
 // unit_done(j) runs after each unit.
-constexpr int kWideStages = 3;
+#ifndef PS_WIDE_STAGES
+#define PS_WIDE_STAGES 3
+#endif
+constexpr int kWideStages = PS_WIDE_STAGES;  // weight chunks in flight: kWideStages - 1 ahead
+// weight rows per warp in the wide GEMM (x 16 tokens): 8 rows halve the staged-x
+// shared-memory reads per FMA against 4 (one 256-thread CTA per SM)
+#ifndef PS_WIDE_R
+#define PS_WIDE_R 8
+#endif
+constexpr int kWideR = PS_WIDE_R;
 template <int TT, int R, int U, class Epi, class UnitDone>
 __device__ __forceinline__ void wide_walk(const float* __restrict__ W, int N, int K, int kbeg, int nvec, int units,
                                           const float* __restrict__ X, int ldx, int rows, float4* xs4, Epi&& epi,
                                           UnitDone&& unit_done) {
-  static_assert(R * TT == 64, "the transposed butterfly leaves 2 of the 64 sums per lane");
+  static_assert(R * TT % 64 == 0, "the transposed butterfly leaves R * TT / 32 sums per lane");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kmax = (nvec + 31) / 32;  // chunk steps per sub-tile (lanes past nvec%32 skip the last)
   const int my_units = int(blockIdx.x) < units ? (units - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
@@ -179,8 +189,8 @@ __device__ __forceinline__ void wide_walk(const float* __restrict__ W, int N, in
   for (int tt = blockIdx.z * TT; tt < rows; tt += TT * gridDim.z) {
     const int nt = min(TT, rows - tt);
     __syncthreads();
-    issue(0);
-    issue(1);
+#pragma unroll
+    for (int q0 = 0; q0 < kWideStages - 1; ++q0) issue(q0);
     stage_x_async(xs4, X, ldx, kbeg, tt, nt, TT, nvec);  // (waits for every group: chunks 0, 1 too)
     __syncthreads();
     int q = 0;
@@ -191,8 +201,8 @@ __device__ __forceinline__ void wide_walk(const float* __restrict__ W, int N, in
 #pragma unroll
         for (int v = 0; v < R * TT; ++v) a[v] = 0.f;
         for (int k = 0; k < kmax; ++k, ++q) {
-          issue(q + 2);
-          asm volatile("cp.async.wait_group 2;" ::: "memory");
+          issue(q + kWideStages - 1);
+          asm volatile("cp.async.wait_group %0;" ::"n"(kWideStages - 1) : "memory");
           const int c = lane + 32 * k;
           if (c < nvec) {
             const float4* wr = ring + (q % kWideStages) * (R * 32) + lane;
@@ -233,7 +243,7 @@ __device__ __forceinline__ void wide_prefetch(const float* W, int N, int K, int 
 }
 
 template <int TT, int R>
-__global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __restrict__ ctx,
+__global__ void __launch_bounds__(256, R * TT > 64 ? 1 : 2) gemm_f32_wide_kernel(const PassCtx* __restrict__ ctx,
                                                                const float* __restrict__ X, int ldx,
                                                                const float* __restrict__ W, float* __restrict__ part,
                                                                int N, int K, int ksplit) {
@@ -247,9 +257,10 @@ __global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __
   wide_walk<TT, R, 1>(
       W, N, K, kbeg, ksplit >> 2, ntiles, X, ldx, ctx->rows, xs4,
       [&](const float (&a)[R * TT], int nb, int tt, int nt) {
+        constexpr int per = R * TT / 32;  // sums lane l holds: values per*l .. per*l + per - 1
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int v = 2 * lane + jj, i = v / TT, t = v % TT;
+        for (int jj = 0; jj < per; ++jj) {
+          const int v = per * lane + jj, i = v / TT, t = v % TT;
           if (t < nt && nb + i < N) part[(size_t(s) * kMaxWindow + tt + t) * N + nb + i] = a[jj];
         }
       },
@@ -258,14 +269,14 @@ __global__ void __launch_bounds__(256, 2) gemm_f32_wide_kernel(const PassCtx* __
 
 // CTAs per (K-split, token chunk) of a wide GEMM: about two resident CTAs per
 // SM in total, never more than the tiles
-static int wide_gx(int ntiles, int splits, int z) {
+static int wide_gx(int ntiles, int splits, int z, int per_sm = 2) {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
   }
-  const int per = (ntiles + max(1, 2 * sms / (splits * z)) - 1) / max(1, 2 * sms / (splits * z));  // tiles per CTA
+  const int per = (ntiles + max(1, per_sm * sms / (splits * z)) - 1) / max(1, per_sm * sms / (splits * z));  // tiles per CTA
   return (ntiles + per - 1) / per;
 }
 
@@ -274,7 +285,7 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
   const int ksplit = K / splits;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_f32_wide_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_f32_wide_kernel<16, kWideR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(gemm_f32_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
@@ -283,9 +294,9 @@ void launch_gemm_f32(const PassCtx* ctx, int max_rows, const float* X, int ldx, 
                N, K, ksplit);
   } else {
     const int z = (max_rows + 15) / 16;
-    const dim3 grid(wide_gx((N + 31) / 32, splits, z), splits, z);
-    const size_t smem = size_t(ksplit) * 16 * 4 + size_t(8) * kWideStages * 4 * 32 * 16;  // x chunk + weight rings
-    launch_pdl(gemm_f32_wide_kernel<16, 4>, grid, dim3(256), smem, st, ctx, X, ldx, W, part, N, K, ksplit);
+    const dim3 grid(wide_gx((N + 8 * kWideR - 1) / (8 * kWideR), splits, z, kWideR > 4 ? 1 : 2), splits, z);
+    const size_t smem = size_t(ksplit) * 16 * 4 + size_t(8) * kWideStages * kWideR * 32 * 16;  // x chunk + weight rings
+    launch_pdl(gemm_f32_wide_kernel<16, kWideR>, grid, dim3(256), smem, st, ctx, X, ldx, W, part, N, K, ksplit);
   }
 }
 
