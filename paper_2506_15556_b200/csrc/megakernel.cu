@@ -417,7 +417,6 @@ __device__ __forceinline__ void load_rstd(const MegaParams& P, bool from_embed, 
 // still in the layer's QKV phase, only this pass's rows (and q) after the
 // barrier, and unit i+1's loads overlap unit i's math.
 constexpr int kAttnRows = 4;  // query rows per attention unit (share one KV page load)
-constexpr int kMaxUnitList = 32;  // units computed before their counts/merges are flushed
 // wide passes: query rows per unit (one 4-row M-tile per worker warp): 16 when
 // the pass's units fit one round over the grid, else 24 (all 6 worker warps),
 // so long contexts take fewer rounds (attention_rows_wide)
@@ -597,10 +596,8 @@ __device__ __forceinline__ void attention_unit(const MegaParams& P, const AttnUn
   const bool tr = trace_p >= 0 && threadIdx.x == 64;
   const int hd = P.hd, grp = P.heads / P.kv_heads;
   const int t0 = U.t0, t1 = U.t1, kvh = U.kvh, s = U.s;
-  const int tid = threadIdx.x - 64;
   const int nrows = t1 - t0;
   const int npairs = nrows * grp;
-  const int ld = (hd + 8) / 2;  // row stride in 32-bit words
   const uint32_t qbase = smem_u32(A.Q(b)), kbase = smem_u32(A.K(b));
   const uint32_t vbase = smem_u32(A.V(b));
   const uint32_t rs = uint32_t(hd + 8) * 2;  // staged row stride in bytes (conflict-free ldmatrix phases)
@@ -993,7 +990,7 @@ __device__ __forceinline__ void attn_merge_one(const MegaParams& P, int n0, int 
 template <class ES>
 __device__ __forceinline__ void attn_count_merge(const MegaParams& P, int n0, int nunits, int w, int lane, ES& es) {
   const int tid = threadIdx.x - 64;
-  const int hd = P.hd, grp = P.heads / P.kv_heads;
+  const int grp = P.heads / P.kv_heads;
   if (tid < nunits * kAttnRows) {
     const int k = tid / kAttnRows, r = tid % kAttnRows;
     const int t0 = es.ulist[k][0], t1 = es.ulist[k][1], kvh = es.ulist[k][2], s = es.ulist[k][3];
@@ -1148,9 +1145,6 @@ __device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, in
   const int hd = P.hd, half = hd >> 1;
   const int f0 = 4 * lane;
   const int n = tile * 128 + f0;
-  const int r = 0;  // X points at this row's inputs
-  const int rope_row = half * 2;
-  (void)rope_row;
   if (kind == PH_QKV) {
     const int rr = n & (hd - 1), pi0 = rr >> 1;  // features f0, f0+1 = dims pi0, pi0+half; f0+2, f0+3 = pi0+1, ..
     const bool is_q = n < P.qd, is_k = !is_q && n < P.qd + P.kvd;
@@ -1165,7 +1159,7 @@ __device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, in
     const float v2 = epi_scale_bias(acc.z, rs, bias[2]), v3 = epi_scale_bias(acc.w, rs, bias[3]);
     float o0 = v0, o1 = v1, o2 = v2, o3 = v3;
     if (is_q || is_k) {
-      const float4 cs = *reinterpret_cast<const float4*>(X + r * rope_row + 2 * pi0);  // (c, s) of pi0, pi0+1
+      const float4 cs = *reinterpret_cast<const float4*>(X + 2 * pi0);  // (c, s) of pi0, pi0+1 (X: this row's RoPE)
       o0 = rope_even(v0, v1, cs.x, cs.y);
       o1 = rope_odd(v1, v0, cs.x, cs.y);
       o2 = rope_even(v2, v3, cs.z, cs.w);
@@ -1193,7 +1187,7 @@ __device__ __forceinline__ void vec_finish_row(const MegaParams& P, int kind, in
     *reinterpret_cast<__nv_bfloat162*>(P.act + size_t(t) * P.I + tile * 64 + 2 * lane) =
         __floats2bfloat162_rn(swiglu(g0, u0), swiglu(g1, u1));
   } else if (kind == PH_O || kind == PH_D) {
-    const float4 xo = *reinterpret_cast<const float4*>(X + r * 128 + f0);
+    const float4 xo = *reinterpret_cast<const float4*>(X + f0);  // (X: this row's residual)
     const float4 xi = make_float4(__fadd_rn(xo.x, acc.x), __fadd_rn(xo.y, acc.y), __fadd_rn(xo.z, acc.z),
                                   __fadd_rn(xo.w, acc.w));
     *reinterpret_cast<float4*>(P.x + size_t(t) * P.H + n) = xi;
@@ -1254,7 +1248,6 @@ __device__ __forceinline__ void finish_share_vec(const MegaParams& P, int kind, 
   const int tid = threadIdx.x - 64;
   const int np = T.npieces;
   const bool has_x = kind == PH_O || kind == PH_D;
-  const bool has_rope = kind == PH_QKV;
   const int hd = P.hd, half = hd >> 1;
   const int rope_row = half * 2;  // floats per RoPE row (cos, sin pairs)
   // staged per row: the pieces' partials, and for O/D the residual row (its
