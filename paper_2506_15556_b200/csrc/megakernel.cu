@@ -1861,12 +1861,55 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
             if (kind == PH_QKV) prefetch_l1(P.rope + size_t(n0) * (P.hd >> 1) + ((n % P.hd) >> 1));
             if (kind == PH_LM && n < P.vocab_local) prefetch_l1(P.lm_bias + P.v_begin + n);
           }
+          // Wide GU / LM phases, a tile of exactly two pieces: the CTA holding the
+          // tile's first k-blocks (c_first; for it the piece is the last of its
+          // range) finalises the whole tile from its own accumulator plus the
+          // partner's partial, which the partner (c_first + 1, its first piece)
+          // published early in the phase — so neither waits for the other at
+          // the tail. The sum own + partner is the CTA-order sum of the
+          // row-share finalisation and of the decode finaliser (finish_tagged).
+          const bool pair_tile = kWide && !all_split && npieces == 2 && (kind == PH_GU || kind == PH_LM) &&
+                                 rows * 512 <= A.buf;
+          float* const own_s = reinterpret_cast<float*>(A.K(0));
+          float* const mate_s = reinterpret_cast<float*>(A.K(1));
+          if (pair_tile && c == c_first && tid == 0) {
+            // the partner's piece: acquire its arrival, then stage its rows
+            // (bulk copy, overlapping this CTA's last k-blocks)
+            grid_wait(cnt + tile, 1u);
+            fence_proxy_async_global();
+            mbar_expect_tx(wbar, uint32_t(rows) * 512u);
+            bulk_g2s(smem_u32(mate_s), P.part + piece_off_slot(c + 1, 0, 0), uint32_t(rows) * 512u, wbar);
+          }
           const uint32_t b = acc_it & 1, aph = (acc_it >> 1) & 1;
           mbar_wait(acc_full0 + 8 * b, aph);
           tc_fence_after();
           if (tid == 0) stamp(P, p, c, G, 4);
           const uint32_t trow = tmem + b * uint32_t(P.acc_cols) + (uint32_t(q * 32) << 16);
-          if (kWide && npieces == 1 && (kind == PH_GU || kind == PH_LM) && rows * 512 <= 2 * A.buf) {
+          if (pair_tile && c == c_first) {
+            ensure_rstd();
+            for (int c0 = 0; w < 4 && c0 < rows; c0 += 32) {  // TMEM lane quadrants: first 4 warps
+              float v[32];
+              tmem_ld32(trow + c0, v);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j < rows) own_s[(c0 + j) * 128 + m] = v[j];
+            }
+            tc_fence_before();
+            wk_bar();
+            if (tid == 0) mbar_arrive(acc_empty0 + 8 * b);
+            mbar_wait(wbar, wphase);
+            wphase ^= 1u;
+            for (int t = w; t < rows; t += kWorkerWarps) {
+              float4 acc = *reinterpret_cast<const float4*>(own_s + t * 128 + 4 * lane);
+              const float4 o = *reinterpret_cast<const float4*>(mate_s + t * 128 + 4 * lane);
+              acc.x += o.x;
+              acc.y += o.y;
+              acc.z += o.z;
+              acc.w += o.w;
+              vec_finish_row(P, kind, layer, n0, w, lane, tile, t, acc, own_s, es);
+            }
+            wk_bar();  // the staging areas are reused by the next tile
+          } else if (kWide && npieces == 1 && (kind == PH_GU || kind == PH_LM) && rows * 512 <= 2 * A.buf) {
             // whole tile of a wide pass: accumulators -> smem [row][128] (a
             // transpose through the idle attention buffers), TMEM released, then
             // the vectorised row math (4 features per thread, as finish_share_vec)
@@ -1939,7 +1982,8 @@ __global__ void __launch_bounds__(kWide ? 256 : 192, 1) mega_kernel(const __grid
             if (!all_split) wk_bar();
             // finalisation is deferred until all of this CTA's pieces are
             // published, so a tile's finaliser never delays the next tile's piece
-            if (spread || es.flag) {
+            // (a two-piece GU / LM tile is finalised by its c_first instead)
+            if (!pair_tile && (spread || es.flag)) {
               if (dtile0 < 0) dtile0 = tile; else dtile1 = tile;
             }
           }
