@@ -905,7 +905,7 @@ __device__ __forceinline__ void attn_merge_load(const MegaParams& P, int n0, int
       L.o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (L.base + u) * hd + lane * 4));
 }
 
-// Any context length: pages beyond the first 8 / 32 are streamed in batches.
+// More than 8 pages: pages beyond the first 8 are streamed in batches of 8.
 __device__ __forceinline__ void attn_merge_general(const MegaParams& P, int lane, const MergeLoad& L) {
   const int hd = P.hd, nsplit = L.nsplit;
   const size_t base = L.base;
@@ -917,26 +917,41 @@ __device__ __forceinline__ void attn_merge_general(const MegaParams& P, int lane
   for (int sp = lane + 32; sp < nsplit; sp += 32)
     Lp += __ldcg(P.ml_part + (base + sp) * 2 + 1) * ex2(__ldcg(P.ml_part + (base + sp) * 2) - M);
   const float Ls = warp_sum(Lp);
-  for (int d4 = lane * 4; d4 < hd; d4 += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp0 = 0; sp0 < nsplit; sp0 += 8) {
-      float f[8];
-      float4 o[8];
+  // hd <= 128 (ps_create): lane owns dims 4 * lane .. +3. Pages 0-7 come from
+  // the operands attn_merge_load already holds, later pages in batches of 8
+  // with every load of a batch in flight; f of page u is ex2(m_u - M) either way
+  const int d4 = lane * 4;
+  const bool has = d4 < hd;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (sp0 + u < nsplit) {
-          f[u] = ex2(__ldcg(P.ml_part + (base + sp0 + u) * 2) - M);
-          o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp0 + u) * hd + d4));
-        }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (sp0 + u < nsplit) {
-          acc.x = fmaf(o[u].x, f[u], acc.x);
-          acc.y = fmaf(o[u].y, f[u], acc.y);
-          acc.z = fmaf(o[u].z, f[u], acc.z);
-          acc.w = fmaf(o[u].w, f[u], acc.w);
-        }
+  for (int u = 0; u < 8; ++u) {  // nsplit > 8 here
+    const float f = ex2(__shfl_sync(0xffffffffu, L.ml.x, u) - M);
+    if (has) {
+      acc.x = fmaf(L.o[u].x, f, acc.x);
+      acc.y = fmaf(L.o[u].y, f, acc.y);
+      acc.z = fmaf(L.o[u].z, f, acc.z);
+      acc.w = fmaf(L.o[u].w, f, acc.w);
     }
+  }
+  for (int sp0 = 8; has && sp0 < nsplit; sp0 += 8) {
+    float f[8];
+    float4 o[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (sp0 + u < nsplit) {
+        f[u] = ex2(__ldcg(P.ml_part + (base + sp0 + u) * 2) - M);
+        o[u] = __ldcg(reinterpret_cast<const float4*>(P.o_part + (base + sp0 + u) * hd + d4));
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (sp0 + u < nsplit) {
+        acc.x = fmaf(o[u].x, f[u], acc.x);
+        acc.y = fmaf(o[u].y, f[u], acc.y);
+        acc.z = fmaf(o[u].z, f[u], acc.z);
+        acc.w = fmaf(o[u].w, f[u], acc.w);
+      }
+  }
+  if (has) {
     __nv_bfloat16* dst = P.attn + size_t(L.t) * P.qd + size_t(L.h) * hd + d4;
     dst[0] = __float2bfloat16_rn(acc.x / Ls);
     dst[1] = __float2bfloat16_rn(acc.y / Ls);
@@ -948,7 +963,7 @@ __device__ __forceinline__ void attn_merge_general(const MegaParams& P, int lane
 // The same arithmetic from the preloaded operands when nsplit <= 8, hd <= 128.
 __device__ __forceinline__ void attn_merge_finish(const MegaParams& P, int lane, const MergeLoad& L) {
   const int hd = P.hd, nsplit = L.nsplit;
-  if (nsplit > 8 || hd > 128) {
+  if (nsplit > 8) {
     attn_merge_general(P, lane, L);
     return;
   }
