@@ -1,6 +1,6 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool racecheck python tools/sanitize_run.py [f32|bf16|all]
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py [f32|bf16|mid|all]
 
 Exercises every entry point of the C-ABI on the cheap shapes: extend passes
 (several chunks), a fused greedy verify with rollback, top-k verify, graph-
@@ -46,6 +46,10 @@ def main():
         exercise(TINY, 0, use_graphs=False)
     if which in ("bf16", "all"):
         exercise(small_shape(), 1, use_graphs=False)
+    if which in ("mid", "all"):
+        # GU / LM wide enough for two-piece tiles: the c_first pair finalisation
+        # (verify window <= 80 rows) and the row-share scheme (the 90-row extend)
+        exercise(small_shape("mid-bf16", intermediate=9728, vocab=32000), 2, use_graphs=False)
     print("sanitize_run done")
 
 
