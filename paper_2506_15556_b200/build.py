@@ -46,7 +46,9 @@ def _digest() -> str:
     for p in sorted(CSRC.glob("*")) + sorted(INCLUDE.glob("*.h")):
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(" ".join(_flags()).encode())
+    # flags without the checkout's absolute paths: a copy of the tree elsewhere (the
+    # GPU box's snapshot) reuses the library built from the same sources
+    h.update(" ".join(_flags()).replace(str(ROOT), "<root>").encode())
     return h.hexdigest()
 
 
